@@ -1,0 +1,635 @@
+// libtlb200 — host runtime of the fused TLoops evaluator (C-ABI, see include/tlb200.h).
+//
+// The CUDA driver (libcuda.so.1) and NVRTC (libnvrtc.so.12) are dlopen'ed on
+// first use, so the library loads — and compiles kernels — on a machine
+// without a GPU; only module loading and launches need the driver.
+//
+// Reference interfaces replaced (paths relative to the reference checkout):
+//   * emit + nvcc of g_NNNN           pkg/src/tlang/codegen_cuda.py:135-204
+//   * CUDAWrapper_g_NNNN launch       pkg/src/tlang/codegen_cuda.py:182-201
+//   * GPUPointers cache               pkg/src/tlang/codegen_cuda.py:219-291
+//   * tl_call_NNNN host invoker       pkg/src/tlang/registry.py:241-257
+
+#include <cuda.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include "../../include/tlb200.h"
+
+namespace {
+
+// ---------------------------------------------------------------- errors ----
+
+thread_local std::string g_err;
+
+int fail(const char* fmt, ...) {
+  char buf[2048];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return 1;
+}
+
+// ------------------------------------------------------ dynamic symbols ----
+
+// Driver API subset, resolved by explicit (versioned) symbol names.
+struct Driver {
+  void* handle = nullptr;
+  CUresult (*Init)(unsigned) = nullptr;
+  CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+  CUresult (*CtxGetCurrent)(CUcontext*) = nullptr;
+  CUresult (*CtxSetCurrent)(CUcontext) = nullptr;
+  CUresult (*CtxGetDevice)(CUdevice*) = nullptr;
+  CUresult (*DeviceGet)(CUdevice*, int) = nullptr;
+  CUresult (*DeviceGetAttribute)(int*, CUdevice_attribute, CUdevice) = nullptr;
+  CUresult (*DevicePrimaryCtxRetain)(CUcontext*, CUdevice) = nullptr;
+  CUresult (*StreamGetCtx)(CUstream, CUcontext*) = nullptr;
+  CUresult (*StreamCreate)(CUstream*, unsigned) = nullptr;
+  CUresult (*StreamSynchronize)(CUstream) = nullptr;
+  CUresult (*StreamWaitEvent)(CUstream, CUevent, unsigned) = nullptr;
+  CUresult (*EventCreate)(CUevent*, unsigned) = nullptr;
+  CUresult (*EventRecord)(CUevent, CUstream) = nullptr;
+  CUresult (*EventDestroy)(CUevent) = nullptr;
+  CUresult (*ModuleLoadData)(CUmodule*, const void*) = nullptr;
+  CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*FuncGetAttribute)(int*, CUfunction_attribute, CUfunction) = nullptr;
+  CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
+                           unsigned, unsigned, CUstream, void**, void**) = nullptr;
+  CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
+  CUresult (*MemAlloc)(CUdeviceptr*, size_t) = nullptr;
+  CUresult (*MemFree)(CUdeviceptr) = nullptr;
+  CUresult (*MemcpyHtoD)(CUdeviceptr, const void*, size_t) = nullptr;
+  CUresult (*MemcpyHtoDAsync)(CUdeviceptr, const void*, size_t, CUstream) = nullptr;
+  CUresult (*MemcpyDtoHAsync)(void*, CUdeviceptr, size_t, CUstream) = nullptr;
+};
+
+// NVRTC subset (the nvrtcProgram handle is an opaque pointer).
+typedef void* nvrtcProgram_t;
+struct Nvrtc {
+  void* handle = nullptr;
+  int (*Version)(int*, int*) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  int (*CreateProgram)(nvrtcProgram_t*, const char*, const char*, int, const char* const*,
+                       const char* const*) = nullptr;
+  int (*CompileProgram)(nvrtcProgram_t, int, const char* const*) = nullptr;
+  int (*GetProgramLogSize)(nvrtcProgram_t, size_t*) = nullptr;
+  int (*GetProgramLog)(nvrtcProgram_t, char*) = nullptr;
+  int (*GetCUBINSize)(nvrtcProgram_t, size_t*) = nullptr;
+  int (*GetCUBIN)(nvrtcProgram_t, char*) = nullptr;
+  int (*DestroyProgram)(nvrtcProgram_t*) = nullptr;
+};
+
+Driver g_cu;
+Nvrtc g_rtc;
+std::mutex g_init_mu;
+bool g_driver_ok = false, g_nvrtc_ok = false;
+
+template <typename F>
+bool bind(void* h, F& fn, const char* name) {
+  fn = reinterpret_cast<F>(dlsym(h, name));
+  return fn != nullptr;
+}
+
+int load_nvrtc_locked() {
+  if (g_nvrtc_ok) return 0;
+  // the toolkit's NVRTC first (matches the nvcc that built this library)
+  const char* names[] = {"/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12",
+                         "libnvrtc.so", nullptr};
+  for (int i = 0; names[i] && !g_rtc.handle; ++i)
+    g_rtc.handle = dlopen(names[i], RTLD_NOW | RTLD_GLOBAL);
+  if (!g_rtc.handle) return fail("tlb: cannot dlopen libnvrtc.so.12: %s", dlerror());
+  void* h = g_rtc.handle;
+  bool ok = bind(h, g_rtc.Version, "nvrtcVersion") &&
+            bind(h, g_rtc.GetErrorString, "nvrtcGetErrorString") &&
+            bind(h, g_rtc.CreateProgram, "nvrtcCreateProgram") &&
+            bind(h, g_rtc.CompileProgram, "nvrtcCompileProgram") &&
+            bind(h, g_rtc.GetProgramLogSize, "nvrtcGetProgramLogSize") &&
+            bind(h, g_rtc.GetProgramLog, "nvrtcGetProgramLog") &&
+            bind(h, g_rtc.GetCUBINSize, "nvrtcGetCUBINSize") &&
+            bind(h, g_rtc.GetCUBIN, "nvrtcGetCUBIN") &&
+            bind(h, g_rtc.DestroyProgram, "nvrtcDestroyProgram");
+  if (!ok) return fail("tlb: libnvrtc lacks a required symbol");
+  g_nvrtc_ok = true;
+  return 0;
+}
+
+int load_driver_locked() {
+  if (g_driver_ok) return 0;
+  if (!g_cu.handle) g_cu.handle = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+  if (!g_cu.handle)
+    return fail("tlb: no CUDA driver (dlopen libcuda.so.1 failed: %s) — a B200 is required",
+                dlerror());
+  void* h = g_cu.handle;
+  bool ok = bind(h, g_cu.Init, "cuInit") && bind(h, g_cu.GetErrorString, "cuGetErrorString") &&
+            bind(h, g_cu.CtxGetCurrent, "cuCtxGetCurrent") &&
+            bind(h, g_cu.CtxSetCurrent, "cuCtxSetCurrent") &&
+            bind(h, g_cu.CtxGetDevice, "cuCtxGetDevice") &&
+            bind(h, g_cu.DeviceGet, "cuDeviceGet") &&
+            bind(h, g_cu.DeviceGetAttribute, "cuDeviceGetAttribute") &&
+            bind(h, g_cu.DevicePrimaryCtxRetain, "cuDevicePrimaryCtxRetain") &&
+            bind(h, g_cu.StreamGetCtx, "cuStreamGetCtx") &&
+            bind(h, g_cu.StreamCreate, "cuStreamCreate") &&
+            bind(h, g_cu.StreamSynchronize, "cuStreamSynchronize") &&
+            bind(h, g_cu.StreamWaitEvent, "cuStreamWaitEvent") &&
+            bind(h, g_cu.EventCreate, "cuEventCreate") &&
+            bind(h, g_cu.EventRecord, "cuEventRecord") &&
+            bind(h, g_cu.EventDestroy, "cuEventDestroy_v2") &&
+            bind(h, g_cu.ModuleLoadData, "cuModuleLoadData") &&
+            bind(h, g_cu.ModuleGetFunction, "cuModuleGetFunction") &&
+            bind(h, g_cu.FuncGetAttribute, "cuFuncGetAttribute") &&
+            bind(h, g_cu.LaunchKernel, "cuLaunchKernel") &&
+            bind(h, g_cu.OccupancyMaxActiveBlocksPerMultiprocessor,
+                 "cuOccupancyMaxActiveBlocksPerMultiprocessor") &&
+            bind(h, g_cu.MemAlloc, "cuMemAlloc_v2") && bind(h, g_cu.MemFree, "cuMemFree_v2") &&
+            bind(h, g_cu.MemcpyHtoD, "cuMemcpyHtoD_v2") &&
+            bind(h, g_cu.MemcpyHtoDAsync, "cuMemcpyHtoDAsync_v2") &&
+            bind(h, g_cu.MemcpyDtoHAsync, "cuMemcpyDtoHAsync_v2");
+  if (!ok) return fail("tlb: libcuda.so.1 lacks a required symbol");
+  CUresult r = g_cu.Init(0);
+  if (r != CUDA_SUCCESS) return fail("tlb: cuInit failed (%d)", (int)r);
+  g_driver_ok = true;
+  return 0;
+}
+
+int ensure(bool driver) {
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (load_nvrtc_locked() && !driver) return 1;
+  if (driver) return load_driver_locked();
+  return 0;
+}
+
+int cu_check(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return 0;
+  const char* s = nullptr;
+  if (g_cu.GetErrorString) g_cu.GetErrorString(r, &s);
+  return fail("tlb: %s failed: %s (%d)", what, s ? s : "?", (int)r);
+}
+
+#define CU(call, what)                          \
+  do {                                          \
+    if (cu_check((call), (what))) return 1;     \
+  } while (0)
+
+// Resolve (and make current) the context a launch on `stream` must use.
+int bind_context(void* stream, CUcontext* out) {
+  CUcontext ctx = nullptr;
+  if (stream) {
+    CU(g_cu.StreamGetCtx((CUstream)stream, &ctx), "cuStreamGetCtx");
+  } else {
+    CU(g_cu.CtxGetCurrent(&ctx), "cuCtxGetCurrent");
+    if (!ctx) {
+      CUdevice dev;
+      CU(g_cu.DeviceGet(&dev, 0), "cuDeviceGet");
+      CU(g_cu.DevicePrimaryCtxRetain(&ctx, dev), "cuDevicePrimaryCtxRetain");
+    }
+  }
+  CUcontext cur = nullptr;
+  g_cu.CtxGetCurrent(&cur);
+  if (cur != ctx) CU(g_cu.CtxSetCurrent(ctx), "cuCtxSetCurrent");
+  *out = ctx;
+  return 0;
+}
+
+// --------------------------------------------------- per-context state ----
+
+struct CtxState {
+  int sm_count = 0;
+  CUstream side[2] = {nullptr, nullptr};
+  CUdeviceptr scratch = 0;
+  size_t scratch_bytes = 0;
+};
+std::mutex g_ctx_mu;
+std::map<CUcontext, CtxState> g_ctx;
+
+int ctx_state(CUcontext ctx, CtxState** out) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  CtxState& st = g_ctx[ctx];
+  if (!st.sm_count) {
+    CUdevice dev;
+    CU(g_cu.CtxGetDevice(&dev), "cuCtxGetDevice");
+    CU(g_cu.DeviceGetAttribute(&st.sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev),
+       "cuDeviceGetAttribute");
+  }
+  *out = &st;
+  return 0;
+}
+
+// ---------------------------------------------------------------- kernel ----
+
+enum Entry { FLAT_V1 = 0, FLAT_V2, BATCH_V1, BATCH_V2, N_ENTRIES };
+const char* kEntryNames[N_ENTRIES] = {"tlk_flat_v1", "tlk_flat_v2", "tlk_batch_v1",
+                                      "tlk_batch_v2"};
+
+struct Loaded {
+  CUmodule mod = nullptr;
+  CUfunction fn[N_ENTRIES] = {};
+  int occ[N_ENTRIES] = {};  // resident blocks per SM at kDefaultThreads
+};
+
+constexpr int kDefaultThreads = 256;
+
+}  // namespace
+
+struct tlb_kernel {
+  std::vector<char> cubin;
+  std::string log;
+  int nfields = 0;
+  std::vector<int> slot_field;
+  std::vector<long long> slot_comp;
+  std::vector<int> slot_flags;
+  std::mutex mu;
+  std::map<CUcontext, Loaded> loaded;
+};
+
+struct tlb_batch {
+  tlb_kernel* k = nullptr;
+  CUcontext ctx = nullptr;
+  CUdeviceptr table = 0;
+  int ndom = 0;
+  long long max_n = 0;
+  bool vec2 = false;
+};
+
+namespace {
+
+int load_module(tlb_kernel* k, CUcontext ctx, Loaded** out) {
+  std::lock_guard<std::mutex> lk(k->mu);
+  auto it = k->loaded.find(ctx);
+  if (it != k->loaded.end()) {
+    *out = &it->second;
+    return 0;
+  }
+  Loaded L;
+  CU(g_cu.ModuleLoadData(&L.mod, k->cubin.data()), "cuModuleLoadData");
+  for (int e = 0; e < N_ENTRIES; ++e) {
+    CU(g_cu.ModuleGetFunction(&L.fn[e], L.mod, kEntryNames[e]), kEntryNames[e]);
+    CU(g_cu.OccupancyMaxActiveBlocksPerMultiprocessor(&L.occ[e], L.fn[e], kDefaultThreads, 0),
+       "cuOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (L.occ[e] < 1) L.occ[e] = 1;
+  }
+  *out = &(k->loaded[ctx] = L);
+  return 0;
+}
+
+bool file_exists(const char* p) {
+  struct stat sb;
+  return p && *p && stat(p, &sb) == 0 && S_ISREG(sb.st_mode);
+}
+
+bool read_file(const char* p, std::vector<char>* out) {
+  FILE* f = fopen(p, "rb");
+  if (!f) return false;
+  fseek(f, 0, SEEK_END);
+  long sz = ftell(f);
+  fseek(f, 0, SEEK_SET);
+  out->resize(sz > 0 ? (size_t)sz : 0);
+  bool ok = sz > 0 && fread(out->data(), 1, (size_t)sz, f) == (size_t)sz;
+  fclose(f);
+  return ok;
+}
+
+void write_file_atomic(const char* p, const std::vector<char>& data) {
+  std::string tmp = std::string(p) + ".tmp." + std::to_string((long)getpid());
+  FILE* f = fopen(tmp.c_str(), "wb");
+  if (!f) return;  // cache is best effort
+  bool ok = fwrite(data.data(), 1, data.size(), f) == data.size();
+  ok = (fclose(f) == 0) && ok;
+  if (ok) rename(tmp.c_str(), p);
+  else unlink(tmp.c_str());
+}
+
+// Per-slot device addresses of one grid from field bases and pitches.
+int resolve_slots(const tlb_kernel* k, const void* const* bases, const long long* pitches,
+                  uint64_t* out, bool* aligned16) {
+  bool al = true;
+  for (size_t j = 0; j < k->slot_field.size(); ++j) {
+    int f = k->slot_field[j];
+    if (!bases[f]) return fail("tlb: field %d has a null base pointer", f);
+    uint64_t a = (uint64_t)(uintptr_t)bases[f] +
+                 (uint64_t)(k->slot_comp[j] * pitches[f]) * sizeof(double);
+    out[j] = a;
+    al = al && (a % 16 == 0);
+  }
+  *aligned16 = al;
+  return 0;
+}
+
+}  // namespace
+
+void tlb_internal_set_error(const char* msg) { g_err = std::string("tlb: ") + msg; }
+
+// ================================================================ C-ABI ====
+
+extern "C" {
+
+int tlb_abi_version(void) { return TLB_ABI_VERSION; }
+
+int tlb_init(int want_driver) { return ensure(want_driver != 0); }
+
+const char* tlb_last_error(void) { return g_err.c_str(); }
+
+int tlb_nvrtc_version(int* major, int* minor) {
+  if (ensure(false)) return 1;
+  int r = g_rtc.Version(major, minor);
+  return r ? fail("tlb: nvrtcVersion failed (%d)", r) : 0;
+}
+
+int tlb_device_sm_count(int* out) {
+  if (ensure(true)) return 1;
+  CUcontext ctx;
+  if (bind_context(nullptr, &ctx)) return 1;
+  CtxState* st;
+  if (ctx_state(ctx, &st)) return 1;
+  *out = st->sm_count;
+  return 0;
+}
+
+int tlb_compile(const char* src, const char* const* opts, int nopts, const char* cache_path,
+                tlb_kernel** out) {
+  if (!src || !out) return fail("tlb_compile: null argument");
+  std::unique_ptr<tlb_kernel> k(new tlb_kernel);
+  if (file_exists(cache_path) && read_file(cache_path, &k->cubin)) {
+    *out = k.release();
+    return 0;
+  }
+  if (ensure(false)) return 1;
+  nvrtcProgram_t prog = nullptr;
+  int r = g_rtc.CreateProgram(&prog, src, "tlb_fused.cu", 0, nullptr, nullptr);
+  if (r) return fail("tlb: nvrtcCreateProgram: %s", g_rtc.GetErrorString(r));
+  r = g_rtc.CompileProgram(prog, nopts, opts);
+  size_t log_size = 0;
+  g_rtc.GetProgramLogSize(prog, &log_size);
+  if (log_size > 1) {
+    k->log.resize(log_size);
+    g_rtc.GetProgramLog(prog, &k->log[0]);
+    k->log.resize(strlen(k->log.c_str()));
+  }
+  if (r) {
+    std::string msg = "tlb: NVRTC compile failed: " + std::string(g_rtc.GetErrorString(r)) +
+                      "\n" + k->log;
+    g_rtc.DestroyProgram(&prog);
+    g_err = msg;
+    return 1;
+  }
+  size_t n = 0;
+  g_rtc.GetCUBINSize(prog, &n);
+  if (n == 0) {
+    g_rtc.DestroyProgram(&prog);
+    return fail("tlb: NVRTC produced no cubin (is --gpu-architecture a real sm_ target?)");
+  }
+  k->cubin.resize(n);
+  g_rtc.GetCUBIN(prog, k->cubin.data());
+  g_rtc.DestroyProgram(&prog);
+  if (cache_path && *cache_path) write_file_atomic(cache_path, k->cubin);
+  *out = k.release();
+  return 0;
+}
+
+const char* tlb_kernel_log(const tlb_kernel* k) { return k ? k->log.c_str() : ""; }
+
+int tlb_kernel_cubin(const tlb_kernel* k, const void** data, long long* size) {
+  if (!k) return fail("tlb_kernel_cubin: null kernel");
+  *data = k->cubin.data();
+  *size = (long long)k->cubin.size();
+  return 0;
+}
+
+void tlb_kernel_destroy(tlb_kernel* k) { delete k; }  // modules live until process exit
+
+int tlb_kernel_set_slots(tlb_kernel* k, int nfields, int nslots, const int* slot_field,
+                         const long long* slot_comp, const int* slot_flags) {
+  if (!k || nfields < 0 || nslots < 1) return fail("tlb_kernel_set_slots: bad arguments");
+  for (int j = 0; j < nslots; ++j)
+    if (slot_field[j] < 0 || slot_field[j] >= nfields || slot_comp[j] < 0)
+      return fail("tlb_kernel_set_slots: slot %d out of range", j);
+  k->nfields = nfields;
+  k->slot_field.assign(slot_field, slot_field + nslots);
+  k->slot_comp.assign(slot_comp, slot_comp + nslots);
+  k->slot_flags.assign(slot_flags, slot_flags + nslots);
+  return 0;
+}
+
+int tlb_kernel_attrs(tlb_kernel* k, const char* entry, int* regs, int* local_bytes,
+                     int* max_threads) {
+  if (ensure(true)) return 1;
+  CUcontext ctx;
+  if (bind_context(nullptr, &ctx)) return 1;
+  Loaded* L;
+  if (load_module(k, ctx, &L)) return 1;
+  for (int e = 0; e < N_ENTRIES; ++e) {
+    if (strcmp(entry, kEntryNames[e])) continue;
+    CU(g_cu.FuncGetAttribute(regs, CU_FUNC_ATTRIBUTE_NUM_REGS, L->fn[e]), "attr regs");
+    CU(g_cu.FuncGetAttribute(local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, L->fn[e]),
+       "attr local");
+    CU(g_cu.FuncGetAttribute(max_threads, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, L->fn[e]),
+       "attr threads");
+    return 0;
+  }
+  return fail("tlb_kernel_attrs: unknown entry %s", entry);
+}
+
+namespace {
+
+int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n, const uint64_t* slots,
+                bool vec2, int threads, long long max_blocks, CUstream stream) {
+  const size_t m = k->slot_field.size();
+  // parameter block: { long long n; double* p[m]; } — passed by value
+  std::vector<uint64_t> param(1 + m);
+  param[0] = (uint64_t)n;
+  memcpy(&param[1], slots, m * sizeof(uint64_t));
+  const int e = vec2 ? FLAT_V2 : FLAT_V1;
+  if (threads <= 0) threads = kDefaultThreads;
+  long long units = vec2 ? n / 2 : n;
+  if (units < 1) units = 1;
+  long long blocks = (units + threads - 1) / threads;
+  long long cap = max_blocks > 0 ? max_blocks
+                                 : (long long)st->sm_count * L->occ[e] *
+                                       (threads == kDefaultThreads ? 1 : 1);
+  if (max_blocks <= 0 && threads != kDefaultThreads) {
+    int occ = 0;
+    g_cu.OccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn[e], threads, 0);
+    cap = (long long)st->sm_count * std::max(occ, 1);
+  }
+  blocks = std::max(1LL, std::min(blocks, cap));
+  void* args[] = {param.data()};
+  CU(g_cu.LaunchKernel(L->fn[e], (unsigned)blocks, 1, 1, (unsigned)threads, 1, 1, 0, stream,
+                       args, nullptr),
+     "cuLaunchKernel(flat)");
+  return 0;
+}
+
+}  // namespace
+
+int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
+               const long long* pitches, int vec, int threads, long long max_blocks,
+               void* stream) {
+  if (!k || k->slot_field.empty()) return fail("tlb_launch: kernel has no slots");
+  if (n < 0) return fail("tlb_launch: negative point count");
+  if (n == 0) return 0;
+  if (ensure(true)) return 1;
+  CUcontext ctx;
+  if (bind_context(stream, &ctx)) return 1;
+  CtxState* st;
+  if (ctx_state(ctx, &st)) return 1;
+  Loaded* L;
+  if (load_module(k, ctx, &L)) return 1;
+  std::vector<uint64_t> slots(k->slot_field.size());
+  bool al;
+  if (resolve_slots(k, field_bases, pitches, slots.data(), &al)) return 1;
+  bool vec2 = vec == 2 ? true : (vec == 1 ? false : al);
+  if (vec2 && !al) return fail("tlb_launch: vec=2 requested but a slot is not 16-byte aligned");
+  return launch_flat(k, L, st, n, slots.data(), vec2, threads, max_blocks, (CUstream)stream);
+}
+
+int tlb_batch_create(tlb_kernel* k, int ndom, const void* const* field_bases,
+                     const long long* pitches, const long long* ns, tlb_batch** out) {
+  if (!k || k->slot_field.empty() || ndom < 1) return fail("tlb_batch_create: bad arguments");
+  if (ensure(true)) return 1;
+  CUcontext ctx;
+  if (bind_context(nullptr, &ctx)) return 1;
+  const size_t m = k->slot_field.size();
+  const int nf = k->nfields;
+  // device record per domain: { long long n; double* p[m]; }
+  std::vector<uint64_t> table((size_t)ndom * (1 + m));
+  bool all_al = true;
+  long long max_n = 0;
+  for (int d = 0; d < ndom; ++d) {
+    uint64_t* rec = &table[(size_t)d * (1 + m)];
+    rec[0] = (uint64_t)ns[d];
+    bool al;
+    if (resolve_slots(k, field_bases + (size_t)d * nf, pitches + (size_t)d * nf, rec + 1, &al))
+      return 1;
+    all_al = all_al && al;
+    max_n = std::max(max_n, ns[d]);
+  }
+  std::unique_ptr<tlb_batch> b(new tlb_batch);
+  b->k = k;
+  b->ctx = ctx;
+  b->ndom = ndom;
+  b->max_n = max_n;
+  b->vec2 = all_al;
+  CU(g_cu.MemAlloc(&b->table, table.size() * sizeof(uint64_t)), "cuMemAlloc(batch table)");
+  CU(g_cu.MemcpyHtoD(b->table, table.data(), table.size() * sizeof(uint64_t)),
+     "cuMemcpyHtoD(batch table)");
+  *out = b.release();
+  return 0;
+}
+
+int tlb_batch_launch(tlb_batch* b, int threads, void* stream) {
+  if (!b) return fail("tlb_batch_launch: null batch");
+  if (ensure(true)) return 1;
+  CUcontext ctx;
+  if (bind_context(stream, &ctx)) return 1;
+  if (ctx != b->ctx) return fail("tlb_batch_launch: stream belongs to another context");
+  CtxState* st;
+  if (ctx_state(ctx, &st)) return 1;
+  Loaded* L;
+  if (load_module(b->k, ctx, &L)) return 1;
+  const int e = b->vec2 ? BATCH_V2 : BATCH_V1;
+  if (threads <= 0) threads = kDefaultThreads;
+  long long units = b->vec2 ? (b->max_n + 1) / 2 : b->max_n;
+  long long gx = std::max(1LL, (units + threads - 1) / threads);
+  long long gy = std::min<long long>(b->ndom, 65535);
+  // cap the total grid at a few waves; blocks loop over x chunks and domains
+  long long cap = (long long)st->sm_count * L->occ[e] * 4;
+  if (gx * gy > cap) gx = std::max(1LL, cap / gy);
+  CUdeviceptr table = b->table;
+  int ndom = b->ndom;
+  void* args[] = {&table, &ndom};
+  CU(g_cu.LaunchKernel(L->fn[e], (unsigned)gx, (unsigned)gy, 1, (unsigned)threads, 1, 1, 0,
+                       (CUstream)stream, args, nullptr),
+     "cuLaunchKernel(batch)");
+  return 0;
+}
+
+void tlb_batch_destroy(tlb_batch* b) {
+  if (!b) return;
+  if (b->table && g_driver_ok) {
+    CUcontext cur = nullptr;
+    g_cu.CtxGetCurrent(&cur);
+    if (cur != b->ctx) g_cu.CtxSetCurrent(b->ctx);
+    g_cu.MemFree(b->table);
+    if (cur && cur != b->ctx) g_cu.CtxSetCurrent(cur);
+  }
+  delete b;
+}
+
+int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_ptrs,
+                  long long slab, void* stream) {
+  if (!k || k->slot_field.empty()) return fail("tlb_exec_host: kernel has no slots");
+  if (n < 0) return fail("tlb_exec_host: negative point count");
+  if (n == 0) return 0;
+  if (ensure(true)) return 1;
+  CUcontext ctx;
+  if (bind_context(stream, &ctx)) return 1;
+  CtxState* st;
+  if (ctx_state(ctx, &st)) return 1;
+  Loaded* L;
+  if (load_module(k, ctx, &L)) return 1;
+  const size_t m = k->slot_field.size();
+  if (slab <= 0) {
+    // two buffers of m*slab doubles, at most ~2 GiB in total
+    long long cap = (1LL << 31) / (long long)(2 * m * sizeof(double));
+    slab = std::min<long long>(n, std::max<long long>(1 << 16, cap));
+  }
+  slab = std::min(slab, n);
+  slab = (slab + 255) / 256 * 256;  // keeps every slot slice 2 KiB aligned
+  std::lock_guard<std::mutex> lk(g_ctx_mu);  // one staged run per process at a time
+  size_t need = 2 * m * (size_t)slab * sizeof(double);
+  if (st->scratch_bytes < need) {
+    if (st->scratch) g_cu.MemFree(st->scratch);
+    st->scratch = 0;
+    st->scratch_bytes = 0;
+    CU(g_cu.MemAlloc(&st->scratch, need), "cuMemAlloc(staging)");
+    st->scratch_bytes = need;
+  }
+  for (int s = 0; s < 2; ++s)
+    if (!st->side[s]) CU(g_cu.StreamCreate(&st->side[s], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+  // order after prior work of the caller's stream
+  CUevent ev;
+  CU(g_cu.EventCreate(&ev, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  CU(g_cu.EventRecord(ev, (CUstream)stream), "cuEventRecord");
+  for (int s = 0; s < 2; ++s) CU(g_cu.StreamWaitEvent(st->side[s], ev, 0), "cuStreamWaitEvent");
+  g_cu.EventDestroy(ev);
+  std::vector<uint64_t> slots(m);
+  long long slab_idx = 0;
+  for (long long lo = 0; lo < n; lo += slab, ++slab_idx) {
+    const long long cnt = std::min(slab, n - lo);
+    const int b = (int)(slab_idx & 1);
+    CUstream s = st->side[b];
+    CUdeviceptr buf = st->scratch + (size_t)b * m * (size_t)slab * sizeof(double);
+    for (size_t j = 0; j < m; ++j) {
+      slots[j] = buf + j * (size_t)slab * sizeof(double);
+      if (k->slot_flags[j] & TLB_SLOT_READ) {
+        const double* src = comp_ptrs[k->slot_field[j]][k->slot_comp[j]] + lo;
+        CU(g_cu.MemcpyHtoDAsync(slots[j], src, (size_t)cnt * sizeof(double), s), "H2D");
+      }
+    }
+    if (launch_flat(k, L, st, cnt, slots.data(), true, 0, 0, s)) return 1;
+    for (size_t j = 0; j < m; ++j) {
+      if (k->slot_flags[j] & TLB_SLOT_WRITE) {
+        double* dst = const_cast<double*>(comp_ptrs[k->slot_field[j]][k->slot_comp[j]]) + lo;
+        CU(g_cu.MemcpyDtoHAsync(dst, slots[j], (size_t)cnt * sizeof(double), s), "D2H");
+      }
+    }
+  }
+  for (int s = 0; s < 2; ++s) CU(g_cu.StreamSynchronize(st->side[s]), "cuStreamSynchronize");
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,172 @@
+// tlk_template.cuh — hand-written sm_100a template for fused TLoops kernels.
+//
+// lowering.py generates, per assignment (or per program of assignments), a
+// straight-line per-point body `tlk_point<T>(P, x)` in SSA form: every input
+// component is loaded once into a register, the right-hand side runs in the
+// reference's exact parse-tree / left-associated-sum order, and each written
+// component is stored once.  This file supplies everything around it:
+//
+//   * T = double  (one point per thread step) or
+//     T = double2 (two consecutive points: 128-bit LDG/STG per component);
+//   * streaming loads/stores (evict-first: every byte is touched once);
+//   * four entry points:
+//       tlk_flat_v1 / tlk_flat_v2   one grid, per-slot base pointers passed
+//                                   by value in the parameter block (constant
+//                                   bank) — no device pointer arrays, which
+//                                   the paper names as its main loss
+//                                   (PAPER.md:1813-1823);
+//       tlk_batch_v1 / tlk_batch_v2 many subdomains in ONE launch: block row
+//                                   y walks domains, the domain's slot
+//                                   pointers are staged in shared memory.
+//   * grid-stride loops over 64-bit point indices (no N <= 65535*bx cap,
+//     reference codegen_cuda.py:187-189).
+//
+// Bit-exactness: compiled with --fmad=false (no DFMA contraction) and IEEE
+// division/sqrt, so each generated operation rounds exactly like the
+// reference's numpy float64 ufunc (pkg/src/tlang/evaluator.py:122-161).
+//
+// lowering.py prepends `#define TLK_NSLOTS <number of pointer slots>` and
+// replaces the @@TLK_BODY@@ marker line below with the per-point body
+// `template <typename T, typename P> tlk_point(const P& P_, long long x)`,
+// which addresses slot j as `P_.p[j] + x`.
+
+#ifndef TLK_THREADS
+#define TLK_THREADS 256
+#endif
+
+// ----------------------------------------------------------- lane arithmetic
+__device__ __forceinline__ double2 operator+(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 operator-(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 operator*(double2 a, double2 b) { return make_double2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ double2 operator/(double2 a, double2 b) { return make_double2(a.x / b.x, a.y / b.y); }
+__device__ __forceinline__ double2 operator+(double a, double2 b) { return make_double2(a + b.x, a + b.y); }
+__device__ __forceinline__ double2 operator-(double a, double2 b) { return make_double2(a - b.x, a - b.y); }
+__device__ __forceinline__ double2 operator*(double a, double2 b) { return make_double2(a * b.x, a * b.y); }
+__device__ __forceinline__ double2 operator/(double a, double2 b) { return make_double2(a / b.x, a / b.y); }
+__device__ __forceinline__ double2 operator+(double2 a, double b) { return make_double2(a.x + b, a.y + b); }
+__device__ __forceinline__ double2 operator-(double2 a, double b) { return make_double2(a.x - b, a.y - b); }
+__device__ __forceinline__ double2 operator*(double2 a, double b) { return make_double2(a.x * b, a.y * b); }
+__device__ __forceinline__ double2 operator/(double2 a, double b) { return make_double2(a.x / b, a.y / b); }
+__device__ __forceinline__ double2 operator-(double2 a) { return make_double2(-a.x, -a.y); }
+__device__ __forceinline__ double tl_sqrt(double a) { return sqrt(a); }
+__device__ __forceinline__ double2 tl_sqrt(double2 a) { return make_double2(sqrt(a.x), sqrt(a.y)); }
+
+template <typename T> __device__ __forceinline__ T tl_splat(double c);
+template <> __device__ __forceinline__ double tl_splat<double>(double c) { return c; }
+template <> __device__ __forceinline__ double2 tl_splat<double2>(double c) { return make_double2(c, c); }
+
+// ------------------------------------------------------------ memory access
+// TLK_LDMODE 0: ld.global.cs (streaming)            [default]
+//            1: ld.global.nc.L1::no_allocate (read-only path, no L1 fill)
+//            2: plain ld.global
+#ifndef TLK_LDMODE
+#define TLK_LDMODE 0
+#endif
+// TLK_STMODE 0: st.global.cs (streaming)            [default]
+//            1: plain st.global
+#ifndef TLK_STMODE
+#define TLK_STMODE 0
+#endif
+
+template <typename T> __device__ __forceinline__ T tl_ld(const double* p);
+template <> __device__ __forceinline__ double tl_ld<double>(const double* p) {
+#if TLK_LDMODE == 0
+  return __ldcs(p);
+#elif TLK_LDMODE == 1
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return *p;
+#endif
+}
+template <> __device__ __forceinline__ double2 tl_ld<double2>(const double* p) {
+#if TLK_LDMODE == 0
+  return __ldcs(reinterpret_cast<const double2*>(p));
+#elif TLK_LDMODE == 1
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+#else
+  return *reinterpret_cast<const double2*>(p);
+#endif
+}
+
+__device__ __forceinline__ void tl_st(double* p, double v) {
+#if TLK_STMODE == 0
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ void tl_st(double* p, double2 v) {
+#if TLK_STMODE == 0
+  __stcs(reinterpret_cast<double2*>(p), v);
+#else
+  *reinterpret_cast<double2*>(p) = v;
+#endif
+}
+
+// ------------------------------------------------------- generated body
+// @@TLK_BODY@@
+
+// ------------------------------------------------------------- entry points
+struct tlk_flat_params {
+  long long n;
+  double* p[TLK_NSLOTS];
+};
+
+struct tlk_shared_ptrs {
+  double* const* p;
+};
+
+extern "C" __global__ void __launch_bounds__(TLK_THREADS)
+tlk_flat_v1(const tlk_flat_params prm) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < prm.n; x += stride)
+    tlk_point<double>(prm, x);
+}
+
+extern "C" __global__ void __launch_bounds__(TLK_THREADS)
+tlk_flat_v2(const tlk_flat_params prm) {
+  const long long pairs = prm.n >> 1;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride)
+    tlk_point<double2>(prm, i << 1);
+  if ((prm.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) tlk_point<double>(prm, prm.n - 1);
+}
+
+// table: per domain { long long n; double* p[TLK_NSLOTS]; } (tlb_batch_create)
+template <typename T>
+__device__ __forceinline__ void tlk_batch_body(const long long* __restrict__ table, int ndom) {
+  __shared__ double* sp[TLK_NSLOTS];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int d = blockIdx.y; d < ndom; d += gridDim.y) {
+    const long long* rec = table + (long long)d * (TLK_NSLOTS + 1);
+    __syncthreads();  // readers of the previous domain's pointers are done
+    for (int j = threadIdx.x; j < TLK_NSLOTS; j += blockDim.x)
+      sp[j] = reinterpret_cast<double*>(rec[1 + j]);
+    const long long n = rec[0];
+    __syncthreads();
+    const tlk_shared_ptrs P{sp};
+    if constexpr (sizeof(T) == 16) {
+      const long long pairs = n >> 1;
+      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride)
+        tlk_point<T>(P, i << 1);
+      if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) tlk_point<double>(P, n - 1);
+    } else {
+      for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += stride)
+        tlk_point<double>(P, x);
+    }
+  }
+}
+
+extern "C" __global__ void __launch_bounds__(TLK_THREADS)
+tlk_batch_v1(const long long* __restrict__ table, int ndom) {
+  tlk_batch_body<double>(table, ndom);
+}
+
+extern "C" __global__ void __launch_bounds__(TLK_THREADS)
+tlk_batch_v2(const long long* __restrict__ table, int ndom) {
+  tlk_batch_body<double2>(table, ndom);
+}

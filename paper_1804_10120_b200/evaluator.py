@@ -1,0 +1,442 @@
+"""Evaluate entry points: run validated statements on the GPU, in place.
+
+Mirror of the reference's ``tlang.evaluator`` (pkg/src/tlang/evaluator.py):
+``eval_statement(v, env, *, chunk=None, threads=None)`` and
+``eval_statement_per_component(v, env)`` keep their signatures, their
+mutate-``env``-in-place contract and their error behaviour (``EvalError``
+for a missing field, disagreeing gridsizes, or an augmented assignment
+that would have to resize; IEEE inf/nan are never errors; ``=`` resizes the
+target, zero-filled, before evaluating — evaluator.py:164-201).
+
+What changes is the execution: each call is ONE launch of the statement's
+fused sm_100a kernel (lowering.py) over the whole grid, on the current torch
+stream of the fields' device.  Fields may also be host-resident (this
+package's fields with ``device="cpu"``, or the reference's own numpy-backed
+``TensorField``): they are then staged through the GPU by the C-ABI
+(``tlb_exec_host``: H2D → kernel → D2H in pipelined slabs).  There is no CPU
+arithmetic path.
+
+Additive extensions (SURVEY.md 8b "API gap"):
+
+* ``eval_program(vs, env)`` — a list of statements fused into ONE kernel
+  (intermediate values stay in registers; each written component is stored
+  once), bit-identical to calling ``eval_statement`` in order;
+* ``eval_batch(vs, envs)`` — the same statements over many independent
+  subdomains in ONE launch (device domain table), bit-identical to looping
+  over ``envs``;
+* ``capture_graph(fn)`` — a CUDA graph of any sequence of the above.
+"""
+
+from __future__ import annotations
+
+import threading
+from typing import Any, Mapping, Sequence
+
+import numpy as np
+
+from . import lowering
+from .lowering import KernelPlan, LoweringError, kind, lower_program
+from .runtime import Batch, Kernel, get_kernel
+
+
+class EvalError(RuntimeError):
+    pass
+
+
+Env = Mapping[str, Any]
+
+
+# ----------------------------------------------- host-side tree transforms --
+# (API mirror of evaluator.py:53-113; the device path resolves sums while
+# lowering and never materialises the expanded tree.)
+
+
+def substitute(e, var, value: int):
+    """Replace every free occurrence of `var` by the fixed value `value`
+    (an inner Sum over `var` shadows it)."""
+    from .ir import Add, Div, Fixed, Leaf, Mul, Neg, Sqrt, Sub, Sum, TensorLeaf, VarTerm
+
+    k = kind(e)
+    if k == "Leaf":
+        def sub(terms):
+            return tuple(Fixed(value + t.offset) if kind(t) == "VarTerm" and t.var == var else t
+                         for t in terms)
+
+        lf = e.leaf
+        outer, inner = sub(lf.outer), sub(lf.inner)
+        if outer == lf.outer and inner == lf.inner:
+            return e
+        return Leaf(TensorLeaf(lf.field, outer, inner, lf.declared_sym))
+    if k in ("Const", "FieldRef"):
+        return e
+    if k in ("Add", "Sub", "Mul", "Div"):
+        cls = {"Add": Add, "Sub": Sub, "Mul": Mul, "Div": Div}[k]
+        return cls(substitute(e.l, var, value), substitute(e.r, var, value))
+    if k in ("Neg", "Sqrt"):
+        return (Neg if k == "Neg" else Sqrt)(substitute(e.e, var, value))
+    if k == "Sum":
+        return e if e.var == var else Sum(e.var, substitute(e.body, var, value))
+    raise TypeError(f"not an expression node: {e!r}")
+
+
+def expand_sum(e):
+    """One Sum as the left-associated chain body[0] + body[1] + ..."""
+    from .ir import Add
+
+    out = substitute(e.body, e.var, 0)
+    for value in range(1, e.var.dim):
+        out = Add(out, substitute(e.body, e.var, value))
+    return out
+
+
+def expand_all_sums(e):
+    """Recursively expand every Sum, outermost first."""
+    from .ir import Add, Div, Mul, Neg, Sqrt, Sub
+
+    k = kind(e)
+    if k == "Sum":
+        return expand_all_sums(expand_sum(e))
+    if k in ("Add", "Sub", "Mul", "Div"):
+        cls = {"Add": Add, "Sub": Sub, "Mul": Mul, "Div": Div}[k]
+        return cls(expand_all_sums(e.l), expand_all_sums(e.r))
+    if k in ("Neg", "Sqrt"):
+        return (Neg if k == "Neg" else Sqrt)(expand_all_sums(e.e))
+    return e
+
+
+# ---------------------------------------------------------- field access --
+
+
+def _lookup(env: Env, name: str):
+    try:
+        return env[name]
+    except KeyError:
+        raise EvalError(f"{name!r} is not present in the data environment") from None
+
+
+def _is_tensor_field(f) -> bool:
+    return hasattr(f, "shape") and hasattr(f, "data") and getattr(f.data, "ndim", 0) == 3
+
+
+def _rhs_names(v) -> list[str]:
+    out, seen = [], set()
+    stack = [v.stmt.rhs]
+    while stack:  # preorder, left to right (ir.walk)
+        e = stack.pop()
+        k = kind(e)
+        name = e.leaf.field if k == "Leaf" else (e.name if k == "FieldRef" else None)
+        if name is not None and name not in seen:
+            seen.add(name)
+            out.append(name)
+        if k in ("Add", "Sub", "Mul", "Div"):
+            stack += [e.r, e.l]
+        elif k in ("Neg", "Sqrt"):
+            stack.append(e.e)
+        elif k == "Sum":
+            stack.append(e.body)
+    return out
+
+
+def _prepare(v, env: Env) -> tuple[Any, int]:
+    """Gridsize agreement; resize the target on plain assignment
+    (reference evaluator.py:180-201, same messages)."""
+    lhs = _lookup(env, v.stmt.lhs.field)
+    if not _is_tensor_field(lhs):
+        raise EvalError(f"{v.stmt.lhs.field!r} is not a tensor field")
+    sizes = {}
+    for name in _rhs_names(v):
+        sizes[name] = _lookup(env, name).gridsize
+    if len(set(sizes.values())) > 1:
+        detail = ", ".join(f"{n}={s}" for n, s in sizes.items())
+        raise EvalError(f"right-hand-side fields disagree on gridsize: {detail}")
+    n = next(iter(sizes.values())) if sizes else lhs.gridsize
+    if sizes and n == 0:
+        raise EvalError(f"field {next(iter(sizes))!r} used in arithmetic before it holds data")
+    if lhs.gridsize != n:
+        if v.stmt.op != "=":
+            raise EvalError(f"{v.stmt.lhs.field!r} has gridsize {lhs.gridsize} but the "
+                            f"right-hand side has {n}; {v.stmt.op} cannot resize")
+        lhs.resize(n)
+    return lhs, n
+
+
+class _Storage:
+    """Where one field's numbers are and how its components are laid out."""
+
+    __slots__ = ("where", "device", "base", "pitch", "comp_ptrs", "ncomp", "key")
+
+    def __init__(self, field, ncomp_expected: int, name: str):
+        data = field.data
+        if isinstance(data, np.ndarray):
+            if data.dtype != np.float64:
+                raise EvalError(f"field {name!r} must hold float64 data, has {data.dtype}")
+            self.where, self.device = "host", None
+            base = data.ctypes.data
+            strides = [s // 8 for s in data.strides]
+        else:  # torch.Tensor
+            import torch
+
+            if data.dtype != torch.float64:
+                raise EvalError(f"field {name!r} must hold float64 data, has {data.dtype}")
+            self.where = "cuda" if data.is_cuda else "host"
+            self.device = data.device if data.is_cuda else None
+            base = data.data_ptr()
+            strides = list(data.stride())
+        if data.ndim == 1:
+            ncomp, comp_offsets = 1, [0]
+            if data.shape[0] > 1 and strides[0] != 1:
+                raise EvalError(f"field {name!r}: grid dimension must be unit-stride")
+        else:
+            oc, ic, npts = data.shape
+            ncomp = oc * ic
+            if npts > 1 and strides[2] != 1:
+                raise EvalError(f"field {name!r}: grid dimension must be unit-stride")
+            comp_offsets = [o * strides[0] + i * strides[1] for o in range(oc) for i in range(ic)]
+        if ncomp != ncomp_expected:
+            raise EvalError(f"field {name!r} holds {ncomp} component arrays, its declaration "
+                            f"has {ncomp_expected}")
+        self.base = base
+        self.ncomp = ncomp
+        self.comp_ptrs = [base + 8 * off for off in comp_offsets]
+        pitch = comp_offsets[1] - comp_offsets[0] if ncomp > 1 else 0
+        if any(off != c * pitch for c, off in enumerate(comp_offsets)):
+            pitch = -1  # not a uniform pitch: only the host-staged path can bind it
+        self.pitch = pitch
+        self.key = (self.where, base)
+
+
+# ------------------------------------------------------------- plan cache --
+
+
+class _PlanCache:
+    def __init__(self) -> None:
+        self._d: dict = {}
+        self._lock = threading.Lock()
+
+    def get(self, vs: Sequence[Any], alias: tuple, components=None) -> tuple[KernelPlan, Kernel]:
+        key = (tuple(id(v) for v in vs), alias, components)
+        hit = self._d.get(key)
+        if hit is not None:
+            return hit[1], hit[2]
+        try:
+            plan = lower_program(list(vs), dict(alias),
+                                 None if components is None else [set(c) for c in components])
+        except LoweringError as exc:
+            raise EvalError(str(exc)) from exc
+        kern = get_kernel(plan)
+        with self._lock:
+            self._d[key] = (tuple(vs), plan, kern)  # keeps vs alive: ids stay unique
+        return plan, kern
+
+
+_plans = _PlanCache()
+
+
+def _bind(vs: Sequence[Any], env: Env, components=None):
+    """Lower (cached) and resolve every field of the program to storage."""
+    names: list[str] = []
+    seen = set()
+    for v in vs:
+        for name in [v.stmt.lhs.field] + _rhs_names(v):
+            if name not in seen:
+                seen.add(name)
+                names.append(name)
+    fields = {n: _lookup(env, n) for n in names}
+    # names addressing the same storage are one field to the kernel
+    rep: dict[tuple, str] = {}
+    alias = []
+    for n in names:
+        d = fields[n].data
+        host_np = isinstance(d, np.ndarray)
+        key = (d.ctypes.data if host_np else d.data_ptr(), tuple(d.shape))
+        size = d.size if host_np else d.numel()
+        if key[0] and size:
+            r = rep.setdefault(key, n)
+            if r != n:
+                alias.append((n, r))
+    plan, kern = _plans.get(vs, tuple(alias), components)
+    stores = []
+    for info in plan.fields:
+        stores.append(_Storage(fields[info.name], info.n_components, info.name))
+    return plan, kern, stores
+
+
+def _launch(plan: KernelPlan, kern: Kernel, stores: list[_Storage], n: int,
+            spans: Sequence[tuple[int, int]] | None = None) -> None:
+    if n == 0:
+        return
+    wheres = {s.where for s in stores}
+    if len(wheres) > 1:
+        raise EvalError("fields of one evaluation live partly on the GPU and partly on the "
+                        "host; move them to one place first")
+    import torch
+
+    if wheres == {"cuda"}:
+        devs = {s.device for s in stores}
+        if len(devs) > 1:
+            raise EvalError(f"fields of one evaluation live on different GPUs: {devs}")
+        dev = devs.pop()
+        if any(s.pitch < 0 for s in stores):
+            raise EvalError("device fields must have a uniform component pitch "
+                            "(contiguous (outer, inner, N) blocks or slab views of them)")
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            pitches = [s.pitch for s in stores]
+            for lo, hi in spans or [(0, n)]:
+                bases = [s.base + 8 * lo for s in stores]
+                kern.launch(hi - lo, bases, pitches, stream)
+    else:
+        if not torch.cuda.is_available():
+            raise EvalError("host-resident fields are evaluated on the GPU, but no CUDA device "
+                            "is available (there is no CPU fallback)")
+        stream = torch.cuda.current_stream().cuda_stream
+        comp = [s.comp_ptrs for s in stores]
+        if spans is None or len(spans) == 1:
+            kern.exec_host(n, comp, stream)
+        else:
+            for lo, hi in spans:
+                kern.exec_host(hi - lo, [[p + 8 * lo for p in row] for row in comp], stream)
+
+
+# -------------------------------------------------------------- public API --
+
+
+def eval_statement(v, env: Env, *, chunk: int | None = None, threads: int | None = None) -> None:
+    """Execute one statement in place over `env` as one fused GPU launch.
+
+    ``chunk`` partitions the grid into consecutive launches of that many
+    points (results are identical — partitioning is invisible, reference
+    test_evaluator.py:200-211); ``threads`` is accepted for API
+    compatibility and has no effect (the GPU grid is the parallelism).
+    """
+    _, n = _prepare(v, env)
+    plan, kern, stores = _bind([v], env)
+    spans = None
+    if chunk:
+        spans = [(lo, min(lo + chunk, n)) for lo in range(0, n, chunk)]
+    _launch(plan, kern, stores, n, spans)
+
+
+def eval_statement_per_component(v, env: Env) -> None:
+    """The paper's "Arrays" pathway (reference evaluator.py:239-257): one
+    GPU launch per canonical LHS component, each a full grid traversal,
+    in component order.  Bitwise equal to ``eval_statement``."""
+    _, n = _prepare(v, env)
+    count = sum(1 for _ in v.lhs_assignments())
+    for k in range(count):
+        plan, kern, stores = _bind([v], env, components=((k,),))
+        _launch(plan, kern, stores, n)
+
+
+def eval_program(vs: Sequence[Any], env: Env) -> None:
+    """Execute statements in order, fused into ONE kernel when they share a
+    gridsize (else one launch per statement).  Bitwise identical to
+    ``for v in vs: eval_statement(v, env)`` (S11)."""
+    vs = list(vs)
+    if not vs:
+        return
+    sizes = []
+    for k, v in enumerate(vs):
+        try:
+            sizes.append(_prepare(v, env)[1])
+        except EvalError:
+            if k:
+                eval_program(vs[:k], env)  # the reference ran those before failing
+            raise
+    if len(set(sizes)) == 1 and all(_lookup(env, nm).gridsize == sizes[0]
+                                    for v in vs for nm in [v.stmt.lhs.field] + _rhs_names(v)):
+        plan, kern, stores = _bind(vs, env)
+        _launch(plan, kern, stores, sizes[0])
+    else:
+        for v in vs:
+            eval_statement(v, env)
+
+
+class _BatchCache:
+    def __init__(self) -> None:
+        self._d: dict = {}
+
+    def get(self, kern: Kernel, table: tuple) -> Batch:
+        key = (id(kern), table)
+        b = self._d.get(key)
+        if b is None:
+            bases = [[t[0] for t in dom[1]] for dom in table]
+            pitches = [[t[1] for t in dom[1]] for dom in table]
+            ns = [dom[0] for dom in table]
+            b = Batch(kern, bases, pitches, ns)
+            if len(self._d) > 64:
+                self._d.clear()
+            self._d[key] = b
+        return b
+
+
+_batches = _BatchCache()
+
+
+def eval_batch(vs, envs: Sequence[Env]) -> None:
+    """Execute a statement (or a program) over many independent subdomains
+    in ONE launch.  ``envs[d]`` is subdomain d's data environment; the result
+    is bitwise identical to ``for env in envs: eval_program(vs, env)``."""
+    if not isinstance(vs, (list, tuple)):
+        vs = [vs]
+    if not envs:
+        return
+    table = []
+    plan = kern = None
+    written: set = set()
+    shared_write = False
+    for env in envs:
+        sizes = {_prepare(v, env)[1] for v in vs}
+        p, k, stores = _bind(vs, env)
+        if kern is None:
+            plan, kern = p, k
+            wf = {fi for fi, fl in zip(plan.slot_field, plan.slot_flags)
+                  if fl & lowering.SLOT_WRITE}
+        elif k is not kern:
+            raise EvalError("subdomains of one batch must share field shapes and aliasing")
+        if len(sizes) != 1 or any(s.where != "cuda" or s.pitch < 0 for s in stores):
+            table = None
+            break
+        for fi in wf:  # a field written by two subdomains would race
+            shared_write |= stores[fi].key in written
+            written.add(stores[fi].key)
+        table.append((sizes.pop(), tuple((s.base, s.pitch) for s in stores), stores[0].device))
+    if table is None or shared_write or len({t[2] for t in table}) > 1:
+        for env in envs:  # not batchable: sequential launches, same bits
+            eval_program(vs, env)
+        return
+    import torch
+
+    dev = table[0][2]
+    key = tuple((t[0], t[1]) for t in table)
+    with torch.cuda.device(dev):
+        _batches.get(kern, key).launch(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def capture_graph(fn, warmup: int = 1):
+    """Run ``fn`` ``warmup`` times (compiles kernels, uploads batch tables),
+    then capture one call into a CUDA graph; returns the graph — ``.replay()``
+    re-executes every launch of ``fn`` with one host call."""
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    return g
+
+
+def plan_for(vs, env: Env) -> KernelPlan:
+    """The lowered plan (source, slots, algorithmic bytes/flops) of a
+    program over `env`, without running it."""
+    if not isinstance(vs, (list, tuple)):
+        vs = [vs]
+    return _bind(list(vs), env)[0]
+
+
+def kernel_for(vs, env: Env) -> Kernel:
+    if not isinstance(vs, (list, tuple)):
+        vs = [vs]
+    return _bind(list(vs), env)[1]

@@ -1,0 +1,455 @@
+"""Lowering: validated tensor statements → one fused sm_100a kernel.
+
+This is the step the reference performs as text emission
+(``codegen_cuda.emit_cuda``, pkg/src/tlang/codegen_cuda.py:135-204, whose
+kernels are never launched) re-designed around what a B200 wants:
+
+* **one thread step = one grid point (or two, with 128-bit accesses)**, not
+  one thread per (point, LHS component): all canonical LHS components of a
+  point are produced by the same thread, so every input component is
+  loaded from HBM exactly once per point and the reference's sequential
+  component-loop semantics (reads of the target see components written
+  earlier in the loop) hold per point for free;
+* **compile-time index resolution**: LHS bindings are enumerated in
+  ``lhs_assignments`` (iter_canonical) order, Sum indices are substituted
+  while walking (an inner Sum over a bound index shadows it,
+  evaluator.py:83-85), every leaf is resolved to its canonical component
+  ``o*inner_count + i`` (ir.leaf_component) — the kernel holds no index
+  arithmetic and no pointer arrays;
+* **exact arithmetic order**: the RHS is emitted in parse-tree order and a
+  ``Sum`` as the left-associated chain ``body[0] + body[1] + ...``
+  starting from term 0 (evaluator.py:142-146), each operation one IEEE
+  fp64 op; NVRTC runs with ``--fmad=false`` so no DFMA contraction can
+  change a rounding.  Constant-only subtrees are folded *with the very
+  Python/numpy scalar semantics the reference evaluator applies to them*
+  (Python floats, ``np.sqrt`` → ``np.float64``), so even their corner
+  cases (ZeroDivisionError on a literal ``1/0``) match;
+* **register shadow**: within a point, the current value of every
+  (field, component) the program touched lives in an SSA register; later
+  reads (same statement through permuted/symmetric indices, or later
+  statements of a program, S10/S11) read the register, and each written
+  component is stored once, after its last write.  This makes a whole
+  *program* of statements one kernel with the same
+  bits as running the statements one by one;
+* value numbering removes repeated identical operations (bitwise safe: no
+  reassociation, no commutation).
+
+The lowering reads IR nodes by class name and attribute names only, so a
+statement built by the reference ``tlang`` package lowers as well.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+import os
+import struct
+from dataclasses import dataclass, field as dc_field
+from pathlib import Path
+from typing import Any, Mapping, Sequence
+
+import numpy as np
+
+from .symmetry import SymmetrySpec, iter_canonical, slot_index
+
+TEMPLATE_PATH = Path(__file__).with_name("csrc") / "tlk_template.cuh"
+LOWERING_VERSION = "tlk-1"
+MAX_PARAM_SLOTS = 500  # 8 + 8*500 bytes < 4 KiB kernel parameter block
+
+SLOT_READ = 1
+SLOT_WRITE = 2
+
+
+class LoweringError(ValueError):
+    pass
+
+
+# ------------------------------------------------------------ duck typing --
+
+
+def kind(node: Any) -> str:
+    return type(node).__name__
+
+
+def as_sym(sym: Any) -> SymmetrySpec:
+    if sym is None:
+        return SymmetrySpec()
+    if isinstance(sym, SymmetrySpec):
+        return sym
+    return SymmetrySpec(tuple(tuple(p) for p in sym.inequalities))
+
+
+@dataclass(frozen=True)
+class FieldInfo:
+    """A field the kernel touches (program-wide numbering)."""
+
+    name: str
+    is_tensor: bool
+    dim: int = 0
+    outer_rank: int = 0
+    inner_rank: int = 0
+    outer_sym: SymmetrySpec = SymmetrySpec()
+    inner_sym: SymmetrySpec = SymmetrySpec()
+    outer_count: int = 1
+    inner_count: int = 1
+
+    @property
+    def n_components(self) -> int:
+        return self.outer_count * self.inner_count
+
+    def component(self, outer: Sequence[int], inner: Sequence[int]) -> int:
+        o = slot_index(self.dim, self.outer_rank, self.outer_sym, outer)
+        i = slot_index(self.dim, self.inner_rank, self.inner_sym, inner)
+        return o * self.inner_count + i
+
+
+def tensor_info(name: str, shape: Any) -> FieldInfo:
+    from .symmetry import component_count
+
+    osym, isym = as_sym(shape.outer_sym), as_sym(shape.inner_sym)
+    return FieldInfo(
+        name, True, shape.dim, shape.outer_rank, shape.inner_rank, osym, isym,
+        component_count(shape.dim, shape.outer_rank, osym),
+        component_count(shape.dim, shape.inner_rank, isym),
+    )
+
+
+# ---------------------------------------------------------------- SSA IR --
+
+
+@dataclass
+class Instr:
+    op: str  # "ld" | "add" | "sub" | "mul" | "div" | "neg" | "sqrt" | "st"
+    dst: int = -1  # register (not for "st")
+    a: Any = None  # operand: int register or _Lit
+    b: Any = None
+    slot: int = -1  # "ld" / "st"
+
+
+@dataclass(frozen=True)
+class _Lit:
+    """A folded constant, kept as the exact Python object the reference's
+    evaluator would hold (float or np.float64)."""
+
+    value: Any
+
+    def c_text(self) -> str:
+        x = float(self.value)
+        if math.isfinite(x):
+            return f"({x.hex()})"
+        bits = struct.unpack("<q", struct.pack("<d", x))[0]
+        return f"__longlong_as_double({bits}LL)"
+
+
+@dataclass
+class KernelPlan:
+    """Everything a launch needs besides the field addresses."""
+
+    source: str
+    fields: list[FieldInfo]
+    slot_field: list[int]
+    slot_comp: list[int]
+    slot_flags: list[int]
+    flops_per_point: int  # algorithmic: binary ops (+ sqrt) after Sum expansion
+    n_ops: int  # emitted arithmetic instructions after value numbering
+    statements: int
+    key: str = ""
+    lhs_fields: list[int] = dc_field(default_factory=list)
+
+    @property
+    def n_slots(self) -> int:
+        return len(self.slot_field)
+
+    @property
+    def reads(self) -> int:
+        return sum(1 for f in self.slot_flags if f & SLOT_READ)
+
+    @property
+    def writes(self) -> int:
+        return sum(1 for f in self.slot_flags if f & SLOT_WRITE)
+
+    @property
+    def bytes_per_point(self) -> int:
+        """Algorithmic HBM bytes per grid point: each read component once,
+        each written component once (read-modify-write counts twice)."""
+        return 8 * (self.reads + self.writes)
+
+
+# --------------------------------------------------------------- builder --
+
+
+class _Builder:
+    def __init__(self) -> None:
+        self.instrs: list[Instr] = []
+        self.nreg = 0
+        self.vn: dict[tuple, int] = {}
+        self.slots: dict[tuple[int, int], int] = {}
+        self.slot_flags: list[int] = []
+        self.shadow: dict[int, Any] = {}  # slot -> current operand
+        self.flops = 0
+
+    def slot(self, f: int, c: int) -> int:
+        key = (f, c)
+        if key not in self.slots:
+            self.slots[key] = len(self.slots)
+            self.slot_flags.append(0)
+        return self.slots[key]
+
+    def reg(self) -> int:
+        self.nreg += 1
+        return self.nreg - 1
+
+    def read(self, f: int, c: int):
+        s = self.slot(f, c)
+        if s not in self.shadow:
+            r = self.reg()
+            self.instrs.append(Instr("ld", r, slot=s))
+            self.slot_flags[s] |= SLOT_READ
+            self.shadow[s] = r
+        return self.shadow[s]
+
+    def write(self, f: int, c: int, val) -> None:
+        s = self.slot(f, c)
+        self.slot_flags[s] |= SLOT_WRITE
+        self.shadow[s] = val
+        self.instrs.append(Instr("st", a=val, slot=s))
+
+    def binary(self, op: str, a, b):
+        if isinstance(a, _Lit) and isinstance(b, _Lit):
+            return _Lit(_fold_binary(op, a.value, b.value))
+        self.flops += 1
+        key = (op, _vn_key(a), _vn_key(b))
+        r = self.vn.get(key)
+        if r is None:
+            r = self.reg()
+            self.instrs.append(Instr(op, r, a, b))
+            self.vn[key] = r
+        return r
+
+    def unary(self, op: str, a):
+        if isinstance(a, _Lit):
+            if op == "neg":
+                return _Lit(-a.value)
+            with np.errstate(all="ignore"):
+                return _Lit(np.sqrt(a.value))
+        if op == "sqrt":
+            self.flops += 1
+        key = (op, _vn_key(a))
+        r = self.vn.get(key)
+        if r is None:
+            r = self.reg()
+            self.instrs.append(Instr(op, r, a))
+            self.vn[key] = r
+        return r
+
+
+def _vn_key(x):
+    # literals by bit pattern: 0.0 and -0.0 must not be merged
+    if isinstance(x, _Lit):
+        return ("c", struct.pack("<d", float(x.value)))
+    return x
+
+
+def _fold_binary(op: str, x, y):
+    # the reference evaluates literal-only subtrees on Python scalars
+    # (evaluator.py:124-141); reproduce that exactly, exceptions included
+    with np.errstate(all="ignore"):
+        if op == "add":
+            return x + y
+        if op == "sub":
+            return x - y
+        if op == "mul":
+            return x * y
+        return x / y  # ZeroDivisionError for Python-float operands, as in the reference
+
+
+_BIN = {"Add": "add", "Sub": "sub", "Mul": "mul", "Div": "div"}
+
+
+class _Lowerer:
+    def __init__(self, alias: Mapping[str, str] | None):
+        self.b = _Builder()
+        self.fields: list[FieldInfo] = []
+        self.index: dict[str, int] = {}
+        self.alias = dict(alias or {})
+
+    def field(self, name: str, info_fn) -> int:
+        rep = self.alias.get(name, name)
+        k = self.index.get(rep)
+        if k is None:
+            k = len(self.fields)
+            self.index[rep] = k
+            self.fields.append(info_fn(rep))
+        return k
+
+    def tensor(self, v, name: str) -> int:
+        k = self.field(name, lambda n: tensor_info(n, v.decls.tensor(name)))
+        if not self.fields[k].is_tensor:
+            raise LoweringError(f"{name!r} is used as a tensor and as a scalar field")
+        return k
+
+    def scalar(self, name: str) -> int:
+        k = self.field(name, lambda n: FieldInfo(n, False))
+        if self.fields[k].is_tensor:
+            raise LoweringError(f"{name!r} is used as a tensor and as a scalar field")
+        return k
+
+    @staticmethod
+    def term_value(t, binding) -> int:
+        return t.value if kind(t) == "Fixed" else binding[t.var] + t.offset
+
+    def leaf_slot(self, v, leaf, binding) -> tuple[int, int]:
+        f = self.tensor(v, leaf.field)
+        info = self.fields[f]
+        outer = [self.term_value(t, binding) for t in leaf.outer]
+        inner = [self.term_value(t, binding) for t in leaf.inner]
+        return f, info.component(outer, inner)
+
+    def expr(self, v, e, binding):
+        k = kind(e)
+        if k == "Const":
+            return _Lit(e.value)
+        if k == "Leaf":
+            return self.b.read(*self.leaf_slot(v, e.leaf, binding))
+        if k == "FieldRef":
+            return self.b.read(self.scalar(e.name), 0)
+        op = _BIN.get(k)
+        if op is not None:
+            a = self.expr(v, e.l, binding)
+            return self.b.binary(op, a, self.expr(v, e.r, binding))
+        if k == "Neg":
+            return self.b.unary("neg", self.expr(v, e.e, binding))
+        if k == "Sqrt":
+            return self.b.unary("sqrt", self.expr(v, e.e, binding))
+        if k == "Sum":
+            acc = self.expr(v, e.body, {**binding, e.var: 0})
+            for val in range(1, e.var.dim):
+                acc = self.b.binary("add", acc, self.expr(v, e.body, {**binding, e.var: val}))
+            return acc
+        raise LoweringError(f"not an expression node: {e!r}")
+
+    def statement(self, v, only: set[int] | None = None) -> None:
+        stmt = v.stmt
+        lhs = stmt.lhs
+        dims = tuple(var.dim for var in v.lhs_vars)
+        for n, values in enumerate(iter_canonical(dims, as_sym(v.loop_sym))):
+            if only is not None and n not in only:
+                continue
+            binding = dict(zip(v.lhs_vars, values))
+            f, c = self.leaf_slot(v, lhs, binding)
+            rhs = self.expr(v, stmt.rhs, binding)
+            if stmt.op == "=":
+                val = rhs
+            else:
+                cur = self.b.read(f, c)
+                val = self.b.binary(_AUG[stmt.op], cur, rhs)
+            self.b.write(f, c, val)
+
+
+_AUG = {"+=": "add", "-=": "sub", "*=": "mul", "/=": "div"}
+_CSYM = {"add": "+", "sub": "-", "mul": "*", "div": "/"}
+
+
+def _operand(x) -> str:
+    return x.c_text() if isinstance(x, _Lit) else f"v{x}"
+
+
+def _emit_body(instrs: list[Instr], hoist_loads: bool = False) -> list[str]:
+    # keep only the final store of every slot; earlier values were consumed
+    # through the register shadow
+    last = {}
+    for k, ins in enumerate(instrs):
+        if ins.op == "st":
+            last[ins.slot] = k
+    out = ["template <typename T, typename P>",
+           "__device__ __forceinline__ void tlk_point(const P& P_, const long long x) {"]
+    if hoist_loads:
+        # SSA + one load per slot before any store of that slot: loads may
+        # all be issued first (maximum memory-level parallelism)
+        instrs = [i for i in instrs if i.op == "ld"] + [i for i in instrs if i.op != "ld"]
+        last = {ins.slot: k for k, ins in enumerate(instrs) if ins.op == "st"}
+    for k, ins in enumerate(instrs):
+        if ins.op == "ld":
+            out.append(f"  const T v{ins.dst} = tl_ld<T>(P_.p[{ins.slot}] + x);")
+        elif ins.op == "st":
+            if last[ins.slot] != k:
+                continue
+            val = ins.a
+            src = f"tl_splat<T>{val.c_text()}" if isinstance(val, _Lit) else f"v{val}"
+            out.append(f"  tl_st(P_.p[{ins.slot}] + x, {src});")
+        elif ins.op in _CSYM:
+            out.append(f"  const T v{ins.dst} = {_operand(ins.a)} {_CSYM[ins.op]} "
+                       f"{_operand(ins.b)};")
+        elif ins.op == "neg":
+            out.append(f"  const T v{ins.dst} = -{_operand(ins.a)};")
+        elif ins.op == "sqrt":
+            out.append(f"  const T v{ins.dst} = tl_sqrt({_operand(ins.a)});")
+        else:  # pragma: no cover
+            raise LoweringError(f"bad instruction {ins}")
+    out.append("}")
+    return out
+
+
+_TEMPLATE_CACHE: list[str] = []
+
+
+def template_text() -> str:
+    if not _TEMPLATE_CACHE:
+        _TEMPLATE_CACHE.append(TEMPLATE_PATH.read_text())
+    return _TEMPLATE_CACHE[0]
+
+
+def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = None,
+                  components: Sequence[set[int] | None] | None = None,
+                  hoist_loads: bool = False) -> KernelPlan:
+    """Lower validated statements, executed in order per grid point, to one
+    fused kernel.  ``alias`` maps field names to a representative name when
+    several names address the same storage.  ``components`` optionally
+    restricts statement k to the given LHS component ordinals (the paper's
+    per-component "Arrays" pathway, evaluator.py:239-257)."""
+    if not statements:
+        raise LoweringError("nothing to lower: no statements")
+    low = _Lowerer(alias)
+    lhs_fields = []
+    for k, v in enumerate(statements):
+        lhs_fields.append(low.tensor(v, v.stmt.lhs.field))
+        low.statement(v, None if components is None else components[k])
+    b = low.b
+    n_slots = len(b.slots)
+    if n_slots > MAX_PARAM_SLOTS:
+        raise LoweringError(f"program touches {n_slots} component arrays; at most "
+                            f"{MAX_PARAM_SLOTS} fit one kernel parameter block")
+    if n_slots == 0:
+        raise LoweringError("statement writes no component")
+    slot_field = [0] * n_slots
+    slot_comp = [0] * n_slots
+    for (f, c), s in b.slots.items():
+        slot_field[s], slot_comp[s] = f, c
+    body = "\n".join(_emit_body(b.instrs, hoist_loads))
+    header = [f"// generated by paper_1804_10120_b200.lowering ({LOWERING_VERSION})"]
+    for v in statements:
+        header.append("// " + _statement_comment(v))
+    header.append(f"#define TLK_NSLOTS {n_slots}")
+    src = "\n".join(header) + "\n" + template_text().replace("// @@TLK_BODY@@", body)
+    n_ops = sum(1 for i in b.instrs if i.op not in ("ld", "st"))
+    plan = KernelPlan(src, low.fields, slot_field, slot_comp, list(b.slot_flags), b.flops, n_ops,
+                      len(statements), lhs_fields=lhs_fields)
+    plan.key = hashlib.sha256(src.encode()).hexdigest()
+    return plan
+
+
+def _statement_comment(v) -> str:
+    try:
+        from .ir import signature
+
+        return signature(v).replace("\n", " ")
+    except Exception:  # reference-built trees: the comment is informational
+        return repr(v.stmt)[:200]
+
+
+def flops_of(statements: Sequence[Any]) -> int:
+    return lower_program(statements).flops_per_point
+
+
+def env_fingerprint() -> str:
+    return os.environ.get("TLK_DEFINES", "")

@@ -1,0 +1,249 @@
+"""ctypes binding of libtlb200.so (include/tlb200.h) and the kernel cache.
+
+The shared library is built in-tree by ``paper_1804_10120_b200.build`` and
+loaded from this package directory.  There is no fallback: if the library
+or NVRTC or the GPU is missing, the calls below raise ``TlbError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+import threading
+from pathlib import Path
+from typing import Sequence
+
+from .lowering import KernelPlan
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = PKG_DIR / "libtlb200.so"
+DEFAULT_CACHE_DIR = PKG_DIR / "_kcache"
+
+ARCH = "sm_100a"
+BASE_OPTIONS = (
+    f"--gpu-architecture={ARCH}",
+    "--fmad=false",  # bit-exact parity: no DFMA contraction
+    "--prec-div=true",
+    "--prec-sqrt=true",
+    "-std=c++17",
+    "-lineinfo",
+)
+
+EXPORTED = (
+    "tlb_abi_version", "tlb_init", "tlb_last_error", "tlb_nvrtc_version", "tlb_device_sm_count",
+    "tlb_compile", "tlb_kernel_log", "tlb_kernel_cubin", "tlb_kernel_destroy",
+    "tlb_kernel_set_slots", "tlb_kernel_attrs", "tlb_launch", "tlb_batch_create",
+    "tlb_batch_launch", "tlb_batch_destroy", "tlb_exec_host", "tlb_fill_uniform",
+)
+
+
+class TlbError(RuntimeError):
+    """A libtlb200 call failed (message from tlb_last_error)."""
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+c_ll = ctypes.c_longlong
+c_vp = ctypes.c_void_p
+c_int = ctypes.c_int
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise TlbError(
+                    f"{LIB_PATH} is missing: build it with "
+                    "`python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(there is no CPU fallback)")
+            L = ctypes.CDLL(str(LIB_PATH))
+            sig = {
+                "tlb_abi_version": (c_int, []),
+                "tlb_init": (c_int, [c_int]),
+                "tlb_last_error": (ctypes.c_char_p, []),
+                "tlb_nvrtc_version": (c_int, [ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+                "tlb_device_sm_count": (c_int, [ctypes.POINTER(c_int)]),
+                "tlb_compile": (c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p), c_int,
+                                        ctypes.c_char_p, ctypes.POINTER(c_vp)]),
+                "tlb_kernel_log": (ctypes.c_char_p, [c_vp]),
+                "tlb_kernel_cubin": (c_int, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_ll)]),
+                "tlb_kernel_destroy": (None, [c_vp]),
+                "tlb_kernel_set_slots": (c_int, [c_vp, c_int, c_int, ctypes.POINTER(c_int),
+                                                 ctypes.POINTER(c_ll), ctypes.POINTER(c_int)]),
+                "tlb_kernel_attrs": (c_int, [c_vp, ctypes.c_char_p, ctypes.POINTER(c_int),
+                                             ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+                "tlb_launch": (c_int, [c_vp, c_ll, ctypes.POINTER(c_vp), ctypes.POINTER(c_ll),
+                                       c_int, c_int, c_ll, c_vp]),
+                "tlb_batch_create": (c_int, [c_vp, c_int, ctypes.POINTER(c_vp),
+                                             ctypes.POINTER(c_ll), ctypes.POINTER(c_ll),
+                                             ctypes.POINTER(c_vp)]),
+                "tlb_batch_launch": (c_int, [c_vp, c_int, c_vp]),
+                "tlb_batch_destroy": (None, [c_vp]),
+                "tlb_exec_host": (c_int, [c_vp, c_ll, ctypes.POINTER(ctypes.POINTER(c_vp)),
+                                          c_ll, c_vp]),
+                "tlb_fill_uniform": (c_int, [c_vp, c_ll, ctypes.c_ulonglong, ctypes.c_ulonglong,
+                                             c_ll, c_vp]),
+            }
+            for name, (res, args) in sig.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        msg = lib().tlb_last_error().decode(errors="replace")
+        raise TlbError(f"{what}: {msg}" if what else msg)
+
+
+def nvrtc_version() -> tuple[int, int]:
+    a, b = c_int(), c_int()
+    check(lib().tlb_nvrtc_version(ctypes.byref(a), ctypes.byref(b)), "nvrtc version")
+    return a.value, b.value
+
+
+def compile_options() -> list[str]:
+    opts = list(BASE_OPTIONS)
+    threads = int(os.environ.get("TLK_THREADS", "256"))
+    opts.append(f"-DTLK_THREADS={threads}")
+    extra = os.environ.get("TLK_DEFINES", "").split()
+    opts += extra
+    return opts
+
+
+def cache_dir() -> Path:
+    d = Path(os.environ.get("TLB_CACHE_DIR", str(DEFAULT_CACHE_DIR)))
+    try:
+        d.mkdir(parents=True, exist_ok=True)
+    except OSError:
+        pass
+    return d
+
+
+def _arr(ctype, values):
+    return (ctype * len(values))(*values)
+
+
+class Kernel:
+    """A compiled fused kernel (cubin + slot map); modules load per context."""
+
+    def __init__(self, plan: KernelPlan, options: Sequence[str] | None = None):
+        self.plan = plan
+        self.options = list(options) if options is not None else compile_options()
+        L = lib()
+        maj, mnr = nvrtc_version()
+        h = hashlib.sha256()
+        h.update(plan.source.encode())
+        h.update("\0".join(self.options).encode())
+        h.update(f"nvrtc{maj}.{mnr}".encode())
+        self.cache_key = h.hexdigest()
+        path = cache_dir() / f"{self.cache_key}.cubin"
+        opts = _arr(ctypes.c_char_p, [o.encode() for o in self.options])
+        handle = c_vp()
+        check(L.tlb_compile(plan.source.encode(), opts, len(self.options), str(path).encode(),
+                            ctypes.byref(handle)), "tlb_compile")
+        self.handle = handle
+        self.cubin_path = path
+        check(L.tlb_kernel_set_slots(handle, len(plan.fields), plan.n_slots,
+                                     _arr(c_int, plan.slot_field), _arr(c_ll, plan.slot_comp),
+                                     _arr(c_int, plan.slot_flags)), "tlb_kernel_set_slots")
+        self.nfields = len(plan.fields)
+        self.launches = 0
+
+    @property
+    def log(self) -> str:
+        return lib().tlb_kernel_log(self.handle).decode(errors="replace")
+
+    def cubin(self) -> bytes:
+        p, n = c_vp(), c_ll()
+        check(lib().tlb_kernel_cubin(self.handle, ctypes.byref(p), ctypes.byref(n)))
+        return ctypes.string_at(p.value, n.value)
+
+    def attrs(self, entry: str = "tlk_flat_v2") -> dict:
+        r, lb, mt = c_int(), c_int(), c_int()
+        check(lib().tlb_kernel_attrs(self.handle, entry.encode(), ctypes.byref(r),
+                                     ctypes.byref(lb), ctypes.byref(mt)), "tlb_kernel_attrs")
+        return {"registers": r.value, "local_bytes": lb.value, "max_threads": mt.value}
+
+    def launch(self, n: int, bases: Sequence[int], pitches: Sequence[int], stream: int,
+               vec: int = 0, threads: int = 0, max_blocks: int = 0) -> None:
+        check(lib().tlb_launch(self.handle, n, _arr(c_vp, bases), _arr(c_ll, pitches), vec,
+                               threads, max_blocks, stream), "tlb_launch")
+        self.launches += 1
+
+    def exec_host(self, n: int, comp_ptrs: Sequence[Sequence[int]], stream: int,
+                  slab: int = 0) -> None:
+        rows = [_arr(c_vp, list(r)) for r in comp_ptrs]
+        outer = (ctypes.POINTER(c_vp) * len(rows))(
+            *[ctypes.cast(r, ctypes.POINTER(c_vp)) for r in rows])
+        check(lib().tlb_exec_host(self.handle, n, outer, slab, stream), "tlb_exec_host")
+        self.launches += 1
+
+
+class Batch:
+    """Uploaded multi-domain table for one kernel (tlb_batch_*)."""
+
+    def __init__(self, kernel: Kernel, bases: Sequence[Sequence[int]],
+                 pitches: Sequence[Sequence[int]], ns: Sequence[int]):
+        self.kernel = kernel
+        flat_b = [b for row in bases for b in row]
+        flat_p = [p for row in pitches for p in row]
+        h = c_vp()
+        check(lib().tlb_batch_create(kernel.handle, len(ns), _arr(c_vp, flat_b),
+                                     _arr(c_ll, flat_p), _arr(c_ll, list(ns)), ctypes.byref(h)),
+              "tlb_batch_create")
+        self.handle = h
+        self.ndom = len(ns)
+
+    def launch(self, stream: int, threads: int = 0) -> None:
+        check(lib().tlb_batch_launch(self.handle, threads, stream), "tlb_batch_launch")
+        self.kernel.launches += 1
+
+    def __del__(self):
+        try:
+            if self.handle and _lib is not None:
+                _lib.tlb_batch_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_kernels: dict[str, Kernel] = {}
+_kernels_lock = threading.Lock()
+
+
+def get_kernel(plan: KernelPlan) -> Kernel:
+    """Compiled kernel for `plan`, cached in memory by source (and on disk
+    by source + options + NVRTC version)."""
+    key = plan.key + "|" + " ".join(compile_options())
+    k = _kernels.get(key)
+    if k is None:
+        with _kernels_lock:
+            k = _kernels.get(key)
+            if k is None:
+                k = Kernel(plan)
+                _kernels[key] = k
+    return k
+
+
+def all_kernels() -> list[Kernel]:
+    return list(_kernels.values())
+
+
+def fill_uniform(t, seed: int, stream_id: int, offset: int = 0, stream: int | None = None):
+    """Fill a contiguous CUDA float64 tensor with counter-based uniform [0,1)
+    values (tlb_fill_uniform; host twin: oracle/counter_rng.py)."""
+    import torch
+
+    assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+    if stream is None:
+        stream = torch.cuda.current_stream(t.device).cuda_stream
+    with torch.cuda.device(t.device):
+        check(lib().tlb_fill_uniform(t.data_ptr(), t.numel(), seed, stream_id, offset, stream),
+              "tlb_fill_uniform")
