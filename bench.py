@@ -1,0 +1,547 @@
+#!/usr/bin/env python
+"""Benchmark of the fused TLoops evaluator on B200 (driver contract).
+
+Workload (BASELINE.json configs[4], "C5"): the program P2 — Christoffel
+symbols Γ^i_jk (18 components) followed by ∂t g_ij (6 components), one fused
+sm_100a kernel — over 2^28 grid points in total, split into contiguous slabs
+across the N GPUs (one process per GPU, no collective on the data path:
+``scaling: strong``, total work fixed as in the config).  Inputs are
+synthetic counter-based uniform[0,1) values (seed 0xC0FFEE) generated on the
+device; 40 input and 24 output component arrays = 512 algorithmic
+bytes/point = 137 GB per pass at N=1, far above the 126 MB L2 (no flush
+needed).  A "step" is one evaluation of P2 over the whole grid.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+``--impl reference`` times the reference's own CPU implementation of the
+path — its emitted C kernels (oracle/_ref/p2.so, built from /root/reference
+by oracle/build_ref.py) driven through their ``tloops_entries`` table on
+all host cores — on a bounded sample of the same workload.
+
+``--sweep`` (development) prints per-config device timings (C1-C4, the C2
+N sweep) as JSON lines instead of the contract line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "gridpoints/sec and HBM GB/s (fraction of roofline) vs N, fp64, 1/2/4/8 B200"
+SEED = 0xC0FFEE
+C5_POINTS = 1 << 28
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--points", type=int, default=C5_POINTS, help="total grid points")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-slab", type=int, default=1 << 24,
+                    help="points per pinned host slab of the e2e leg")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 22,
+                    help="points of the CPU-baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU work of the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------ distributed --
+
+
+class Dist:
+    def __init__(self):
+        import torch
+
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            torch.cuda.set_device(self.local)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+        else:
+            torch.cuda.set_device(0)
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def allreduce(self, x: float, op: str = "max") -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX if op == "max" else self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+def slab(n_total: int, rank: int, world: int, align: int = 256) -> tuple[int, int]:
+    from paper_1804_10120_b200.partition import slab_bounds
+
+    return slab_bounds(n_total, rank, world, align)
+
+
+# ---------------------------------------------------------------- helpers --
+
+
+def measured_peak() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = Path(f"/tmp/tlb_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        self.path.unlink(missing_ok=True)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_p2_env(n_local: int, lo: int, device: str):
+    """P2 fields of one slab on `device`, inputs counter-RNG filled by global
+    point index (so values do not depend on the partition)."""
+    import torch
+
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.fields import ScalarField, TensorField
+    from paper_1804_10120_b200.runtime import fill_uniform
+
+    prog, vs = tb.load(tb.P2)
+    targets = {v.stmt.lhs.field for v in vs}
+    env = {}
+    sid = 0
+    for item in prog.items:
+        name = getattr(item, "name", None)
+        if name in prog.decls.tensors:
+            f = TensorField(name, prog.decls.tensors[name], n_local, device=device)
+            comps = f.data.view(-1, n_local)
+        elif name in prog.decls.scalar_fields:
+            f = ScalarField(name, n_local, device=device)
+            comps = f.data.view(1, n_local)
+        else:
+            continue
+        if name not in targets:
+            for c in range(comps.shape[0]):
+                fill_uniform(comps[c], SEED, (sid << 8) | c, offset=lo)
+        sid += 1
+        env[name] = f
+    torch.cuda.synchronize()
+    return prog, vs, env
+
+
+# ------------------------------------------------------------ our impl --
+
+
+def run_ours(args, dist: Dist) -> dict | None:
+    import torch
+
+    from paper_1804_10120_b200 import eval_program
+    from paper_1804_10120_b200.evaluator import kernel_for, plan_for
+
+    lo, hi = slab(args.points, dist.rank, dist.world)
+    n_local = hi - lo
+    prog, vs, env = build_p2_env(n_local, lo, "cuda")
+    plan = plan_for(vs, env)
+    kern = kernel_for(vs, env)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        eval_program(vs, env)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(torch.cuda.current_device())
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_begin = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches0 = kern.launches
+    clocks.start()
+    time.sleep(0.3)  # let the sampler take a baseline reading
+    dist.barrier()
+    torch.cuda.synchronize()
+    t_begin.record(stream)
+    for k in range(args.steps):
+        starts[k].record(stream)
+        eval_program(vs, env)
+        ends[k].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    launches = kern.launches - launches0
+    total_ms = t_begin.elapsed_time(t_end)
+    kernel_ms = statistics.mean(s.elapsed_time(e) for s, e in zip(starts, ends))
+    total_ms = dist.allreduce(total_ms, "max")
+    kernel_ms_max = dist.allreduce(kernel_ms, "max")
+    launches = int(dist.allreduce(float(launches), "sum"))
+
+    ms_per_step = total_ms / args.steps
+    value = args.points / (ms_per_step / 1e3)
+    peak, peak_src = measured_peak()
+    alg_bytes = plan.bytes_per_point * n_local  # per launch, this rank
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    achieved = dist.allreduce(achieved, "max") if False else achieved
+    traffic = None
+    tr_path = ROOT / "profiles" / "ncu_traffic.json"
+    if tr_path.exists():
+        try:
+            per_pt = json.loads(tr_path.read_text())["p2"]["dram_bytes_per_point"]
+            traffic = per_pt * n_local
+        except Exception:
+            traffic = None
+
+    e2e = None
+    if not args.no_e2e:
+        del env
+        torch.cuda.empty_cache()
+        e2e = run_e2e(args, dist, vs, n_local)
+
+    cpu = None
+    if not args.no_cpu and dist.world == 1:
+        cpu = cpu_baseline(args)
+
+    if dist.rank != 0:
+        return None
+    return {
+        "metric": METRIC,
+        "value": value,
+        "unit": "gridpoints/s",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: counter-based uniform[0,1) inputs (splitmix64, seed 0xC0FFEE), "
+                "generated on the device",
+        "config": {
+            "workload": "C5: program P2 = Christoffel Gamma^i_jk (18 comps) + dt g_ij "
+                        "(6 comps), one fused kernel, 2^28 points total",
+            "program": "p2",
+            "points_total": args.points,
+            "points_per_gpu": n_local,
+            "partition": "contiguous 256-aligned point slabs per GPU, no collective",
+            "bytes_per_point": plan.bytes_per_point,
+            "flops_per_point": plan.flops_per_point,
+            "arrays": {"read": plan.reads, "written": plan.writes},
+            "l2": "working set 137 GB >> 126 MB L2; no flush needed",
+        },
+        "hbm_gbs": alg_bytes * dist.world / (ms_per_step / 1e3) / 1e9,
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "peak_source": peak_src,
+            "kernel": "tlk_flat_v2 (fused P2)",
+            "kernel_ms": kernel_ms,
+            "kernel_ms_max_over_ranks": kernel_ms_max,
+            "algorithmic_bytes_per_launch": alg_bytes,
+        },
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "gpu_launches": launches,
+    }
+
+
+def run_e2e(args, dist: Dist, vs, n_local: int) -> dict:
+    """Same metric through the public API with HOST fields: each step moves
+    every input component host→device and every output back (pinned host
+    slab of --e2e-slab points reused for all slabs of the grid)."""
+    import torch
+
+    from paper_1804_10120_b200 import eval_program
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.evaluator import plan_for
+
+    s = min(args.e2e_slab, n_local)
+    prog, _ = tb.load(tb.P2)
+    host = tb.make_env(prog, "Gamma", s, SEED, device="cpu")
+    for f in host.values():  # pinned host memory for full-speed async copies
+        f.data = f.data.pin_memory()
+    host["dtg"].data.zero_()
+    plan = plan_for(vs, host)
+    chunks = [(lo, min(lo + s, n_local)) for lo in range(0, n_local, s)]
+    eval_program(vs, host)  # warm-up (staging buffers, module load)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        for lo, hi in chunks:
+            if hi - lo != s:  # ragged tail slab
+                part = {k: _host_view(f, 0, hi - lo) for k, f in host.items()}
+                eval_program(vs, part)
+            else:
+                eval_program(vs, host)
+    torch.cuda.synchronize()
+    dist.barrier()
+    dt = dist.allreduce(time.perf_counter() - t0, "max") / args.e2e_steps
+    h2d = 8 * plan.reads * n_local
+    d2h = 8 * plan.writes * n_local
+    return {"value": args.points / dt, "unit": "gridpoints/s",
+            "h2d_bytes_per_step": h2d * dist.world, "d2h_bytes_per_step": d2h * dist.world,
+            "s_per_step": dt, "steps": args.e2e_steps,
+            "path": "eval_program(host pinned fields) -> tlb_exec_host: H2D -> fused kernel "
+                    "-> D2H, 2-stream slab pipeline",
+            "host_slab_points": s}
+
+
+def _host_view(f, lo, hi):
+    import copy
+
+    g = copy.copy(f)
+    g.data = f.data[..., lo:hi]
+    return g
+
+
+# ------------------------------------------------------- CPU references --
+
+
+def _cpu_sample_env(n: int):
+    import numpy as np
+
+    from paper_1804_10120_b200 import bench as tb
+
+    prog, vs = tb.load(tb.P2)
+    rng = np.random.default_rng(SEED)
+    env = {}
+    for name, shape in prog.decls.tensors.items():
+        env[name] = rng.uniform(0.0, 1.0, (shape.outer_count, shape.inner_count, n))
+    for name in prog.decls.scalar_fields:
+        env[name] = rng.uniform(0.0, 1.0, n)
+    return vs, env
+
+
+def cpu_reference_runner(n: int):
+    """(kind, cores, run()) for the reference CPU implementation on n points."""
+    from oracle import refc
+
+    vs, env = _cpu_sample_env(n)
+    if refc.available("p2"):
+        prog = refc.RefProgram("p2")
+        cores = os.cpu_count() or 1
+        return "reference", cores, (lambda: prog.run(env, n, threads=cores))
+    from oracle import numpy_eval
+
+    return "port", 1, (lambda: numpy_eval.eval_program(vs, env))
+
+
+def cpu_baseline(args) -> dict:
+    kind, cores, go = cpu_reference_runner(args.cpu_sample)
+    go()  # warm (page faults, thread pool)
+    times = []
+    t_all = time.perf_counter()
+    while time.perf_counter() - t_all < args.cpu_seconds and len(times) < 200:
+        t0 = time.perf_counter()
+        go()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    what = ("reference emitted C (codegen_c, cc -O2) via tloops_entries, grid split in "
+            "per-core slabs" if kind == "reference" else "oracle numpy port, 1 thread")
+    return {"value": args.cpu_sample / t, "unit": "gridpoints/s", "cores": cores, "kind": kind,
+            "sample": f"P2 on {args.cpu_sample} points x {len(times)} runs "
+                      f"(median {t * 1e3:.1f} ms/run): {what}"}
+
+
+def run_reference(args, dist: Dist) -> dict | None:
+    if dist.rank != 0:
+        return None
+    kind, cores, go = cpu_reference_runner(args.cpu_sample)
+    for _ in range(args.warmup):
+        go()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        go()
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = args.cpu_sample / (ms / 1e3)
+    sample = (f"P2 on a {args.cpu_sample}-point sample of the 2^28-point workload per step; "
+              + ("reference emitted C (oracle/_ref/p2.so) via tloops_entries, "
+                 f"{cores} host threads" if kind == "reference" else "oracle numpy port"))
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "gridpoints/s",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: uniform[0,1) (numpy default_rng(0xC0FFEE))",
+        "config": {"workload": "C5: program P2 (Christoffel + dt g_ij), reference CPU path",
+                   "program": "p2", "points_total": args.points,
+                   "points_per_step_sample": args.cpu_sample},
+        "cpu_baseline": {"value": value, "unit": "gridpoints/s", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "gridpoints/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+# ---------------------------------------------------------------- sweep --
+
+
+def run_sweep(args) -> None:
+    """Device time per config via CUDA-graph replay (no host overhead)."""
+    import torch
+
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200 import capture_graph, eval_batch, eval_program
+    from paper_1804_10120_b200.evaluator import plan_for
+
+    peak, _ = measured_peak()
+    flush = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")  # 256 MB > L2
+
+    def timed(fn, reps=21, flush_l2=True):
+        g = capture_graph(fn)
+        ts = []
+        for _ in range(reps):
+            if flush_l2:
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+        return statistics.median(ts[1:])
+
+    def report(name, n, t, plan, extra=None):
+        gbs = plan.bytes_per_point * n / t / 1e9
+        line = {"config": name, "N": n, "t_s": t, "gridpoints_per_s": n / t, "hbm_gbs": gbs,
+                "frac": gbs / peak, "bytes_per_point": plan.bytes_per_point}
+        line.update(extra or {})
+        print(json.dumps(line), flush=True)
+
+    for name, text, sizes in (
+            ("C2_maxwell", tb.MAXWELL, [10**3, 10**4, 10**5, 10**6, 10**7, 10**8]),
+            ("C1_dtg", tb.DTG, [64**3, 128**3, 1 << 24]),
+            ("C3_christoffel", tb.CHRISTOFFEL, [64**3, 128**3, 1 << 24]),
+            ("P2", tb.P2, [128**3, 1 << 24]),
+            ("P3", tb.P3, [128**3, 1 << 24])):
+        prog, vs = tb.load(text)
+        for n in sizes:
+            targets = {v.stmt.lhs.field for v in vs}
+            env = tb.make_env(prog, "__none__", 0, SEED)
+            for f in env.values():
+                f.resize(n)
+                if f.name not in targets:
+                    f.data.uniform_()
+            plan = plan_for(vs, env)
+            for l2 in (True, False):
+                t = timed(lambda: eval_program(vs, env), flush_l2=l2)
+                report(name, n, t, plan, {"l2_flushed": l2})
+            del env
+            torch.cuda.empty_cache()
+    # C4: 512 subdomains of 16^3 points, P2 per domain, one launch
+    prog, vs = tb.load(tb.P2)
+    envs = []
+    for d in range(512):
+        env = tb.make_env(prog, "__none__", 0, SEED + d)
+        for f in env.values():
+            f.resize(16**3)
+            if f.name not in ("Gamma", "dtg"):
+                f.data.uniform_()
+        envs.append(env)
+    plan = plan_for(vs, envs[0])
+    t = timed(lambda: eval_batch(vs, envs))
+    report("C4_batch_512x16^3", 512 * 16**3, t, plan, {"launches": 1})
+    t = timed(lambda: [eval_program(vs, e) for e in envs])
+    report("C4_graph_512_launches", 512 * 16**3, t, plan, {"launches": 512})
+
+
+def main() -> int:
+    args = parse_args()
+    if args.sweep:
+        run_sweep(args)
+        return 0
+    dist = Dist()
+    try:
+        line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+    finally:
+        dist.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -118,7 +118,19 @@ def _is_tensor_field(f) -> bool:
     return hasattr(f, "shape") and hasattr(f, "data") and getattr(f.data, "ndim", 0) == 3
 
 
+_NAMES: dict[int, tuple] = {}
+
+
 def _rhs_names(v) -> list[str]:
+    hit = _NAMES.get(id(v))
+    if hit is not None and hit[0] is v:
+        return hit[1]
+    out = _rhs_names_walk(v)
+    _NAMES[id(v)] = (v, out)
+    return out
+
+
+def _rhs_names_walk(v) -> list[str]:
     out, seen = [], set()
     stack = [v.stmt.rhs]
     while stack:  # preorder, left to right (ir.walk)
@@ -163,7 +175,7 @@ def _prepare(v, env: Env) -> tuple[Any, int]:
 class _Storage:
     """Where one field's numbers are and how its components are laid out."""
 
-    __slots__ = ("where", "device", "base", "pitch", "comp_ptrs", "ncomp", "key")
+    __slots__ = ("where", "device", "base", "pitch", "ncomp", "key", "_offsets")
 
     def __init__(self, field, ncomp_expected: int, name: str):
         data = field.data
@@ -172,37 +184,58 @@ class _Storage:
                 raise EvalError(f"field {name!r} must hold float64 data, has {data.dtype}")
             self.where, self.device = "host", None
             base = data.ctypes.data
-            strides = [s // 8 for s in data.strides]
+            strides = [st // 8 for st in data.strides]
         else:  # torch.Tensor
-            import torch
-
-            if data.dtype != torch.float64:
+            if data.dtype is not _f64():
                 raise EvalError(f"field {name!r} must hold float64 data, has {data.dtype}")
-            self.where = "cuda" if data.is_cuda else "host"
-            self.device = data.device if data.is_cuda else None
+            if data.is_cuda:
+                self.where, self.device = "cuda", data.device
+            else:
+                self.where, self.device = "host", None
             base = data.data_ptr()
-            strides = list(data.stride())
-        if data.ndim == 1:
-            ncomp, comp_offsets = 1, [0]
-            if data.shape[0] > 1 and strides[0] != 1:
+            strides = data.stride()
+        shape = data.shape
+        if len(shape) == 1:
+            ncomp, oc, ic = 1, 1, 1
+            if shape[0] > 1 and strides[0] != 1:
                 raise EvalError(f"field {name!r}: grid dimension must be unit-stride")
         else:
-            oc, ic, npts = data.shape
+            oc, ic, npts = shape
             ncomp = oc * ic
             if npts > 1 and strides[2] != 1:
                 raise EvalError(f"field {name!r}: grid dimension must be unit-stride")
-            comp_offsets = [o * strides[0] + i * strides[1] for o in range(oc) for i in range(ic)]
         if ncomp != ncomp_expected:
             raise EvalError(f"field {name!r} holds {ncomp} component arrays, its declaration "
                             f"has {ncomp_expected}")
-        self.base = base
-        self.ncomp = ncomp
-        self.comp_ptrs = [base + 8 * off for off in comp_offsets]
-        pitch = comp_offsets[1] - comp_offsets[0] if ncomp > 1 else 0
-        if any(off != c * pitch for c, off in enumerate(comp_offsets)):
+        if ncomp == 1:
+            pitch = 0
+        elif ic == 1:
+            pitch = strides[0]
+        elif oc == 1 or strides[0] == ic * strides[1]:
+            pitch = strides[1]
+        else:
             pitch = -1  # not a uniform pitch: only the host-staged path can bind it
-        self.pitch = pitch
+        self.base, self.pitch, self.ncomp = base, pitch, ncomp
+        self._offsets = (oc, ic, strides)
         self.key = (self.where, base)
+
+    @property
+    def comp_ptrs(self) -> list[int]:
+        oc, ic, st = self._offsets
+        if len(st) == 1:
+            return [self.base]
+        return [self.base + 8 * (o * st[0] + i * st[1]) for o in range(oc) for i in range(ic)]
+
+
+_F64 = []
+
+
+def _f64():
+    if not _F64:
+        import torch
+
+        _F64.append(torch.float64)
+    return _F64[0]
 
 
 # ------------------------------------------------------------- plan cache --
@@ -279,12 +312,16 @@ def _launch(plan: KernelPlan, kern: Kernel, stores: list[_Storage], n: int,
         if any(s.pitch < 0 for s in stores):
             raise EvalError("device fields must have a uniform component pitch "
                             "(contiguous (outer, inner, N) blocks or slab views of them)")
-        with torch.cuda.device(dev):
-            stream = torch.cuda.current_stream(dev).cuda_stream
-            pitches = [s.pitch for s in stores]
+        pitches = [s.pitch for s in stores]
+        if dev.index == torch.cuda.current_device():
+            stream = torch.cuda.current_stream().cuda_stream
             for lo, hi in spans or [(0, n)]:
-                bases = [s.base + 8 * lo for s in stores]
-                kern.launch(hi - lo, bases, pitches, stream)
+                kern.launch(hi - lo, [s.base + 8 * lo for s in stores], pitches, stream)
+        else:
+            with torch.cuda.device(dev):
+                stream = torch.cuda.current_stream(dev).cuda_stream
+                for lo, hi in spans or [(0, n)]:
+                    kern.launch(hi - lo, [s.base + 8 * lo for s in stores], pitches, stream)
     else:
         if not torch.cuda.is_available():
             raise EvalError("host-resident fields are evaluated on the GPU, but no CUDA device "

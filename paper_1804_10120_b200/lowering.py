@@ -434,7 +434,10 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     n_ops = sum(1 for i in b.instrs if i.op not in ("ld", "st"))
     plan = KernelPlan(src, low.fields, slot_field, slot_comp, list(b.slot_flags), b.flops, n_ops,
                       len(statements), lhs_fields=lhs_fields)
-    plan.key = hashlib.sha256(src.encode()).hexdigest()
+    # identical source text can serve different slot maps (e.g. the
+    # per-component kernels of one statement): the plan identity covers both
+    ident = f"{src}\0{slot_field}\0{slot_comp}\0{plan.slot_flags}"
+    plan.key = hashlib.sha256(ident.encode()).hexdigest()
     return plan
 
 

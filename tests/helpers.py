@@ -67,3 +67,102 @@ def same_bits(a, b) -> bool:
         return False
     eq = a.view(np.uint64) == b.view(np.uint64)
     return bool((eq | (np.isnan(a) & np.isnan(b))).all())
+
+
+class NumpyTensorField:
+    """Stand-in with the reference TensorField's surface (numpy-backed
+    ``data`` (outer, inner, N), ``shape``, ``gridsize``, ``resize``) — what a
+    user of the reference package hands to the drop-in evaluator."""
+
+    def __init__(self, name, shape, data):
+        self.name, self.shape, self.data = name, shape, data
+
+    @property
+    def gridsize(self):
+        return self.data.shape[2]
+
+    def resize(self, n):
+        if n != self.gridsize:
+            self.data = np.zeros(self.data.shape[:2] + (n,))
+
+
+class NumpyScalarField:
+    def __init__(self, name, data):
+        self.name, self.data = name, data
+
+    @property
+    def gridsize(self):
+        return self.data.shape[0]
+
+    def resize(self, n):
+        if n != self.gridsize:
+            self.data = np.zeros(n)
+
+
+def numpy_env(prog, host: dict) -> dict:
+    env = {}
+    for name, shape in prog.decls.tensors.items():
+        env[name] = NumpyTensorField(name, shape, host[name].copy())
+    for name in prog.decls.scalar_fields:
+        env[name] = NumpyScalarField(name, host[name].copy())
+    return env
+
+
+def env_to_host(env: dict) -> dict:
+    out = {}
+    for k, f in env.items():
+        d = f.data
+        out[k] = d.copy() if isinstance(d, np.ndarray) else d.detach().cpu().numpy().copy()
+    return out
+
+
+RANDOM_DECLS = """tensor A dim 3 rank 1;
+tensor B dim 3 rank 2;
+tensor S dim 3 rank 2 sym(0,1);
+tensor D dim 3 rank 2 sym(0,1) inner rank 1;
+tensor T dim 3 rank 2;
+tensor U dim 3 rank 2 sym(0,1);
+field w;
+"""
+
+
+def random_program(rng, n_statements: int = 2) -> str:
+    """Random valid statements over RANDOM_DECLS (free indices i, j)."""
+
+    def scal(depth):
+        opts = ["w", "2.5", "sqrt(w)", "(w + 1)", "Sum(k, A(k))", "-w", "0.125"]
+        if depth > 0:
+            a, b = scal(depth - 1), scal(depth - 1)
+            opts += [f"({a}*{b})", f"({a} - {b})", f"({a}/({b} + 3))"]
+        return opts[rng.integers(len(opts))]
+
+    def vec(depth, sym_ok=True):
+        opts = ["B(i, j)", "B(j, i)", "S(i, j)", "S(j, i)", "A(i)*A(j)", "T(i, j)", "T(j, i)",
+                "U(j, i)", "Sum(k, B(i, k)*B(k, j))", "Sum(k, D(i, j)(k))",
+                "Sum(k, D(i, k)(j)*A(k))", "Sum(l, Sum(k, S(i, k)*B(k, l)*S(l, j)))"]
+        if depth > 0:
+            a, b = vec(depth - 1), vec(depth - 1)
+            s = scal(depth - 1)
+            opts += [f"({a} + {b})", f"({a} - {b})", f"{s}*{a}", f"{a}/({s} + 2)", f"-{a}",
+                     f"{a}*{s}"]
+        return opts[rng.integers(len(opts))]
+
+    lines = []
+    for _ in range(n_statements):
+        target = ["T(i, j)", "U(sym<0,1>, i, j)"][rng.integers(2)]
+        op = ["=", "=", "+=", "-=", "*=", "/="][rng.integers(6)]
+        rhs = scal(2) if op in ("*=", "/=") else vec(2)
+        if op in ("*=", "/="):
+            rhs = f"({rhs} + 1.5)"
+        lines.append(f"{target} {op} {rhs};")
+    return RANDOM_DECLS + "\n".join(lines) + "\n"
+
+
+def random_host_env(prog, n: int, seed: int) -> dict:
+    rng = np.random.default_rng(seed)
+    out = {}
+    for name, shape in prog.decls.tensors.items():
+        out[name] = rng.uniform(0.0, 1.0, (shape.outer_count, shape.inner_count, n))
+    for name in prog.decls.scalar_fields:
+        out[name] = rng.uniform(0.0, 1.0, n)
+    return out

@@ -1,0 +1,193 @@
+"""Device parity: the fused sm_100a kernels against the reference's own
+outputs (golden vectors) and against the CPU oracle.  Bar: bit-exact
+(NaN payloads aside) — the kernels run the reference's exact operation
+order with --fmad=false."""
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import (case_names, device_env, env_to_host, golden_io, manifest, numpy_env,
+                     program, random_host_env, random_program, same_bits)
+from oracle import counter_rng, numpy_eval
+from paper_1804_10120_b200 import (EvalError, capture_graph, eval_batch, eval_program,
+                                   eval_statement, eval_statement_per_component)
+from paper_1804_10120_b200.runtime import all_kernels, fill_uniform
+
+pytestmark = pytest.mark.gpu
+
+CASES = case_names()
+
+
+def _check(case, env_host, want):
+    for t in case["targets"]:
+        assert same_bits(env_host[t], want[t]), t
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fused_program_matches_reference_bitwise(name):
+    case = manifest()["cases"][name]
+    prog, vs = program(case["source"])
+    host, want = golden_io(name)
+    env = device_env(prog, host)
+    eval_program(vs, env)
+    _check(case, env_to_host(env), want)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_statement_by_statement_matches_reference_bitwise(name):
+    case = manifest()["cases"][name]
+    prog, vs = program(case["source"])
+    host, want = golden_io(name)
+    env = device_env(prog, host)
+    for v in vs:
+        eval_statement(v, env)
+    _check(case, env_to_host(env), want)
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if len(manifest()["cases"][n]["statements"]) == 1])
+def test_per_component_arrays_mode_bitwise(name):
+    case = manifest()["cases"][name]
+    prog, (v,) = program(case["source"])
+    host, want = golden_io(name)
+    env = device_env(prog, host)
+    eval_statement_per_component(v, env)
+    _check(case, env_to_host(env), want)
+
+
+@pytest.mark.parametrize("name", ["c1_dtg", "c1_dtg_odd", "c3_christoffel", "c4_p3",
+                                  "seq_augmented", "special_values", "aliased_write_order"])
+def test_host_fields_staged_through_gpu_bitwise(name):
+    # the reference's own numpy-backed fields: drop-in, computed on the GPU
+    case = manifest()["cases"][name]
+    prog, vs = program(case["source"])
+    host, want = golden_io(name)
+    env = numpy_env(prog, host)
+    eval_program(vs, env)
+    _check(case, env_to_host(env), want)
+    env = device_env(prog, host, device="cpu")  # this package's host fields
+    eval_program(vs, env)
+    _check(case, env_to_host(env), want)
+
+
+@pytest.mark.parametrize("name", ["c1_dtg_odd", "c3_christoffel", "suite_contract3"])
+@pytest.mark.parametrize("chunk", [1, 7, 32])
+def test_chunking_is_invisible(name, chunk):
+    case = manifest()["cases"][name]
+    prog, (v,) = program(case["source"])
+    host, want = golden_io(name)
+    env = device_env(prog, host)
+    eval_statement(v, env, chunk=chunk, threads=4)
+    _check(case, env_to_host(env), want)
+
+
+@pytest.mark.parametrize("name", ["c4_p2", "c4_p3", "c2_maxwell", "suite_kij"])
+def test_multi_domain_batch_one_launch(name):
+    case = manifest()["cases"][name]
+    prog, vs = program(case["source"])
+    host, want = golden_io(name)
+    envs = [device_env(prog, host) for _ in range(5)]
+    before = sum(k.launches for k in all_kernels())
+    eval_batch(vs, envs)
+    assert sum(k.launches for k in all_kernels()) == before + 1
+    for env in envs:
+        _check(case, env_to_host(env), want)
+
+
+def test_cuda_graph_replay():
+    case = manifest()["cases"]["c4_p2"]
+    prog, vs = program(case["source"])
+    host, want = golden_io("c4_p2")
+    env = device_env(prog, host)
+    g = capture_graph(lambda: eval_program(vs, env))
+    for t in case["targets"]:
+        env[t].data.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    _check(case, env_to_host(env), want)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_programs_match_oracle(seed):
+    rng = np.random.default_rng(seed)
+    src = random_program(rng, n_statements=1 + seed % 3)
+    prog, vs = program(src)
+    n = [1, 2, 3, 255, 256, 1001][seed % 6]
+    host = random_host_env(prog, n, seed)
+    want = {k: a.copy() for k, a in host.items()}
+    numpy_eval.eval_program(vs, want)
+    env = device_env(prog, host)
+    eval_program(vs, env)
+    got = env_to_host(env)
+    for t in ("T", "U", "A"):
+        assert same_bits(got[t], want[t]), (src, t)
+
+
+def test_large_grid_slab_parity_and_partition_invisibility():
+    # Christoffel + dt g (P2) at 2^22+6 points, counter-RNG inputs; check
+    # three slabs bitwise against the oracle, and that evaluating two slab
+    # views of the same fields gives the same bits as one launch
+    case = manifest()["cases"]["c4_p2"]
+    prog, vs = program(case["source"])
+    n = (1 << 22) + 6
+    env = device_env(prog, {k: np.zeros(a.shape[:-1] + (n,)) for k, a in
+                            golden_io("c4_p2")[0].items()})
+    names = list(prog.decls.tensors) + sorted(prog.decls.scalar_fields)
+    for sid, nm in enumerate(names):
+        fill_uniform(env[nm].data.view(-1), 0xC0FFEE, sid)
+    eval_program(vs, env)
+    got = env_to_host(env)
+    for lo, hi in [(0, 4096), (n // 2 - 1000, n // 2 + 1000), (n - 4096, n)]:
+        host = {}
+        for sid, nm in enumerate(names):
+            full = counter_rng.uniform(0xC0FFEE, sid, 0, env[nm].data.numel())
+            host[nm] = full.reshape(env[nm].data.shape)[..., lo:hi].copy()
+        for t in case["targets"]:
+            host[t][:] = 0.0
+        numpy_eval.eval_program(vs, host)
+        for t in case["targets"]:
+            assert same_bits(got[t][..., lo:hi], host[t]), (t, lo)
+    # partition invisibility: two slab views
+    from paper_1804_10120_b200.fields import ScalarField, TensorField
+
+    def view(f, lo, hi):
+        g = (TensorField if hasattr(f, "shape") else ScalarField)(f.name, *(
+            (f.shape, 0) if hasattr(f, "shape") else (0,)))
+        g.data = f.data[..., lo:hi]
+        return g
+
+    for t in case["targets"]:
+        env[t].data.zero_()
+    cut = (n // 3) & ~1
+    for lo, hi in [(0, cut), (cut, n)]:
+        eval_program(vs, {k: view(f, lo, hi) for k, f in env.items()})
+    again = env_to_host(env)
+    for t in case["targets"]:
+        assert same_bits(again[t], got[t]), t
+
+
+def test_device_rng_matches_host_twin():
+    t = torch.empty(100_003, dtype=torch.float64, device="cuda")
+    fill_uniform(t, 123, 7, offset=999)
+    assert (t.cpu().numpy() == counter_rng.uniform(123, 7, 999, 100_003)).all()
+
+
+def test_resize_and_error_semantics():
+    prog, (v_set, v_add) = program("tensor A dim 3 rank 1;\ntensor B dim 3 rank 1;\n"
+                                   "A(i) = B(i);\nA(i) += B(i);\n")
+    env = device_env(prog, {"A": np.zeros((3, 1, 2)), "B": np.ones((3, 1, 4))})
+    eval_statement(v_set, env)
+    assert env["A"].gridsize == 4 and bool((env["A"].data == 1).all())
+    env["A"].resize(3)
+    with pytest.raises(EvalError, match="cannot resize"):
+        eval_statement(v_add, env)
+    del env["B"]
+    with pytest.raises(EvalError, match="'B'"):
+        eval_statement(v_set, env)
+
+
+def test_empty_grid_is_a_no_op():
+    prog, (v,) = program("tensor A dim 3 rank 1;\nA(i) = 2;\n")
+    env = device_env(prog, {"A": np.zeros((3, 1, 0))})
+    eval_statement(v, env)
+    assert env["A"].gridsize == 0
