@@ -117,6 +117,36 @@ void tlb_batch_destroy(tlb_batch* b);
 int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_ptrs,
                   long long slab, void* stream);
 
+/* ---- reference-harness bindings --------------------------------------------
+ *
+ * Lets the reference's UNCHANGED conformance harness (pkg/harness/tl_harness.c)
+ * drive the fused GPU kernels: paper_1804_10120_b200.registry writes a
+ * tloops_bindings_b200.c whose tloops_entries[] has the reference layout
+ * (pkg/src/tlang/registry.py:134-167) and whose per-entry `call(N, T, S, D)`
+ * forwards to tlb_harness_call with the host pointer arrays the harness
+ * built (flattened, symmetric images aliased — tl_harness.c:200-205).
+ */
+typedef struct tlb_harness_kernel {
+  const char* source;            /* fused kernel source (lowering.py) */
+  int nopts;
+  const char* const* opts;       /* NVRTC options */
+  int nfields;                   /* kernel fields, lowering order */
+  const int* field_kind;         /* 0: tensor argument T[field_arg], 1: scalar S[field_arg] */
+  const int* field_arg;
+  const int* field_ncomp;
+  const long* const* field_comp_flat; /* per tensor field: flat index of each component */
+  int nslots;
+  const int* slot_field;
+  const long long* slot_comp;
+  const int* slot_flags;
+  tlb_kernel* compiled;          /* filled on first call */
+} tlb_harness_kernel;
+
+/* Stage the harness's host arrays through the GPU and run the kernel
+ * (compiling it on first use; cubins cached under $TLB_CACHE_DIR if set). */
+int tlb_harness_call(tlb_harness_kernel* hk, long n, double** const* tensors,
+                     const double* const* scalars);
+
 /* ---- synthetic data ------------------------------------------------------ */
 
 /* dst[i] = u01(seed, stream_id, offset + i) for i in [0, n): a counter-based

@@ -632,4 +632,53 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
   return 0;
 }
 
+int tlb_harness_call(tlb_harness_kernel* hk, long n, double** const* tensors,
+                     const double* const* scalars) {
+  if (!hk) return fail("tlb_harness_call: null kernel");
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!hk->compiled) {
+      // optional on-disk cubin cache keyed by FNV-1a of source + options
+      std::string cache;
+      if (const char* dir = getenv("TLB_CACHE_DIR")) {
+        uint64_t h = 1469598103934665603ull;
+        auto mixin = [&h](const char* p) {
+          for (; *p; ++p) h = (h ^ (unsigned char)*p) * 1099511628211ull;
+          h = (h ^ 0xff) * 1099511628211ull;
+        };
+        mixin(hk->source);
+        for (int i = 0; i < hk->nopts; ++i) mixin(hk->opts[i]);
+        char name[40];
+        snprintf(name, sizeof name, "/harness_%016llx.cubin", (unsigned long long)h);
+        cache = std::string(dir) + name;
+      }
+      tlb_kernel* k = nullptr;
+      if (tlb_compile(hk->source, hk->opts, hk->nopts, cache.empty() ? nullptr : cache.c_str(),
+                      &k))
+        return 1;
+      if (tlb_kernel_set_slots(k, hk->nfields, hk->nslots, hk->slot_field, hk->slot_comp,
+                               hk->slot_flags)) {
+        tlb_kernel_destroy(k);
+        return 1;
+      }
+      hk->compiled = k;
+    }
+  }
+  // host address of every component of every kernel field
+  std::vector<std::vector<const double*>> comps(hk->nfields);
+  std::vector<const double* const*> rows(hk->nfields);
+  for (int f = 0; f < hk->nfields; ++f) {
+    if (hk->field_kind[f] == 1) {
+      comps[f].push_back(scalars[hk->field_arg[f]]);
+    } else {
+      double** const flat = tensors[hk->field_arg[f]];
+      for (int c = 0; c < hk->field_ncomp[f]; ++c)
+        comps[f].push_back(flat[hk->field_comp_flat[f][c]]);
+    }
+    rows[f] = comps[f].data();
+  }
+  return tlb_exec_host(hk->compiled, n, rows.data(), 0, nullptr);
+}
+
 }  // extern "C"

@@ -35,6 +35,7 @@ EXPORTED = (
     "tlb_compile", "tlb_kernel_log", "tlb_kernel_cubin", "tlb_kernel_destroy",
     "tlb_kernel_set_slots", "tlb_kernel_attrs", "tlb_launch", "tlb_batch_create",
     "tlb_batch_launch", "tlb_batch_destroy", "tlb_exec_host", "tlb_fill_uniform",
+    "tlb_harness_call",
 )
 
 

@@ -191,3 +191,33 @@ def test_empty_grid_is_a_no_op():
     env = device_env(prog, {"A": np.zeros((3, 1, 0))})
     eval_statement(v, env)
     assert env["A"].gridsize == 0
+
+
+@pytest.mark.parametrize("case", ["c1_dtg", "c2_maxwell", "c4_p2", "c4_p3", "seq_augmented",
+                                  "special_values"])
+def test_reference_harness_drives_the_gpu_kernels(case, tmp_path):
+    # the reference's own, unchanged tl_harness binary loads
+    # our bindings table and runs every manifest entry on the GPU
+    import subprocess
+
+    from helpers import GOLDEN, read_host
+    from oracle import refc
+    from paper_1804_10120_b200.registry import Registry
+
+    harness = refc.REF_DIR / "tl_harness"
+    if not harness.exists():
+        pytest.skip("oracle/_ref/tl_harness not built")
+    spec = manifest()["cases"][case]
+    _, vs = program(spec["source"])
+    reg = Registry()
+    for v in vs:
+        reg.register(v)
+    so = reg.build_shared(tmp_path)
+    out = tmp_path / "out.tldf"
+    res = subprocess.run([str(harness), str(so), str(tmp_path / "tloops_manifest.tsv"),
+                          str(GOLDEN / f"{case}.in.tldf"), str(out)],
+                         capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr
+    got, want = read_host(out), golden_io(case)[1]
+    for t in spec["targets"]:
+        assert same_bits(got[t], want[t]), t
