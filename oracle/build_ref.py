@@ -15,8 +15,10 @@ are git-ignored but travel to the GPU box with the repo snapshot.
      as its harness does (`cc -shared -fPIC -O2 -std=c99`, tl_harness.c:77):
        _ref/<program>.so            exports tloops_entries / tloops_entry_count
        _ref/<program>.manifest.tsv  ordinal, signature, N_e, N_d
-  3. The reference's CUDA emission for the same programs, kept as source
-     under _ref/<program>_cuda/ (comparator material).
+  3. The reference's CUDA emission for the same programs (the paper's GPU
+     design: one thread per (point, LHS component), device pointer arrays),
+     compiled as-is with nvcc for sm_100a into _ref/<program>_cuda.so — the
+     comparator of SURVEY.md 8f #3 (driven by oracle/refcuda.py).
 
 Usage: python oracle/build_ref.py [--force]
 """
@@ -76,7 +78,8 @@ def build(force: bool = False) -> Path:
     for name, text in programs().items():
         so = OUT / f"{name}.so"
         src_file = OUT / f"{name}.tl"
-        if not force and so.exists() and src_file.exists() and src_file.read_text() == text:
+        fresh = so.exists() and (OUT / f"{name}_cuda.so").exists() and src_file.exists()
+        if not force and fresh and src_file.read_text() == text:
             continue
         res = parse_program(text)
         assert res.ok, res.diagnostics
@@ -94,6 +97,14 @@ def build(force: bool = False) -> Path:
         if cuda.exists():
             shutil.rmtree(cuda)
         reg.write_all(cuda, "cuda")
+        # the paper's GPU design as emitted (comparator):
+        # default nvcc flags, as the reference's own syntax test compiles it
+        # (test_acceptance.py:238-242), for sm_100a
+        nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+        _run([nvcc, "-shared", "-Xcompiler", "-fPIC", "-O3",
+              "-gencode", "arch=compute_100a,code=sm_100a",
+              str(cuda / "tloops_kernels.cu"), str(cuda / "tloops_bindings.cu"),
+              "-o", str(OUT / f"{name}_cuda.so")])
         src_file.write_text(text)
     return OUT
 

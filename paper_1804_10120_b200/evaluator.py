@@ -335,6 +335,70 @@ def _launch(plan: KernelPlan, kern: Kernel, stores: list[_Storage], n: int,
                 kern.exec_host(hi - lo, [[p + 8 * lo for p in row] for row in comp], stream)
 
 
+# -------------------------------------------------------- bound launches --
+# Steady-state fast path: once a program has run over a set of device fields,
+# the launch (kernel, point count, ctypes address arrays) is remembered under
+# the fields' (address, shape, strides).  A later call over the same storage
+# skips _prepare/_bind — their outcome depends only on those shapes — and is
+# a single C call (SURVEY.md 7.3 "host overhead per call").
+
+_FAST: dict = {}
+_FAST_NAMES: dict = {}
+
+
+def _program_names(vs) -> list[str]:
+    key = tuple(id(v) for v in vs)
+    hit = _FAST_NAMES.get(key)
+    if hit is not None:
+        return hit[1]
+    names: list[str] = []
+    for v in vs:
+        for nm in [v.stmt.lhs.field] + _rhs_names(v):
+            if nm not in names:
+                names.append(nm)
+    _FAST_NAMES[key] = (tuple(vs), names)
+    return names
+
+
+def _fast_key(vs, env: Env):
+    parts = []
+    for nm in _program_names(vs):
+        f = env.get(nm) if hasattr(env, "get") else None
+        if f is None:
+            return None
+        d = getattr(f, "data", None)
+        if d is None or isinstance(d, np.ndarray) or not d.is_cuda:
+            return None
+        parts.append((d.data_ptr(), d.shape, d.stride()))
+    return (tuple(id(v) for v in vs), tuple(parts))
+
+
+def _fast_run(key) -> bool:
+    hit = _FAST.get(key)
+    if hit is None:
+        return False
+    import torch
+
+    _vs, kern, n, bases, pitches, dev = hit
+    if dev == torch.cuda.current_device():
+        stream = torch.cuda.current_stream().cuda_stream
+    else:
+        stream = torch.cuda.current_stream(torch.device("cuda", dev)).cuda_stream
+    kern.launch_arrays(n, bases, pitches, stream)
+    return True
+
+
+def _fast_record(key, vs, kern: Kernel, stores: list, n: int) -> None:
+    if key is None or n == 0 or any(s.where != "cuda" or s.pitch < 0 for s in stores):
+        return
+    if len(_FAST) > 512:
+        _FAST.clear()
+    from .runtime import address_arrays
+
+    bases, pitches = address_arrays([s.base for s in stores], [s.pitch for s in stores])
+    _FAST[key] = (tuple(vs), kern, n, bases, pitches, stores[0].device.index)
+
+
 # -------------------------------------------------------------- public API --
 
 
@@ -346,12 +410,18 @@ def eval_statement(v, env: Env, *, chunk: int | None = None, threads: int | None
     test_evaluator.py:200-211); ``threads`` is accepted for API
     compatibility and has no effect (the GPU grid is the parallelism).
     """
+    if not chunk:
+        key = _fast_key((v,), env)
+        if key is not None and _fast_run(key):
+            return
     _, n = _prepare(v, env)
     plan, kern, stores = _bind([v], env)
     spans = None
     if chunk:
         spans = [(lo, min(lo + chunk, n)) for lo in range(0, n, chunk)]
     _launch(plan, kern, stores, n, spans)
+    if not chunk:
+        _fast_record(_fast_key((v,), env), (v,), kern, stores, n)
 
 
 def eval_statement_per_component(v, env: Env) -> None:
@@ -372,6 +442,9 @@ def eval_program(vs: Sequence[Any], env: Env) -> None:
     vs = list(vs)
     if not vs:
         return
+    key = _fast_key(vs, env)
+    if key is not None and _fast_run(key):
+        return
     sizes = []
     for k, v in enumerate(vs):
         try:
@@ -384,6 +457,7 @@ def eval_program(vs: Sequence[Any], env: Env) -> None:
                                     for v in vs for nm in [v.stmt.lhs.field] + _rhs_names(v)):
         plan, kern, stores = _bind(vs, env)
         _launch(plan, kern, stores, sizes[0])
+        _fast_record(_fast_key(vs, env), vs, kern, stores, sizes[0])
     else:
         for v in vs:
             eval_statement(v, env)

@@ -179,6 +179,13 @@ class Kernel:
                                threads, max_blocks, stream), "tlb_launch")
         self.launches += 1
 
+    def launch_arrays(self, n: int, bases, pitches, stream: int) -> None:
+        """Launch with prebuilt ctypes address arrays (bound-launch fast path)."""
+        rc = _lib.tlb_launch(self.handle, n, bases, pitches, 0, 0, 0, stream)
+        if rc:
+            check(rc, "tlb_launch")
+        self.launches += 1
+
     def exec_host(self, n: int, comp_ptrs: Sequence[Sequence[int]], stream: int,
                   slab: int = 0) -> None:
         rows = [_arr(c_vp, list(r)) for r in comp_ptrs]
@@ -186,6 +193,10 @@ class Kernel:
             *[ctypes.cast(r, ctypes.POINTER(c_vp)) for r in rows])
         check(lib().tlb_exec_host(self.handle, n, outer, slab, stream), "tlb_exec_host")
         self.launches += 1
+
+
+def address_arrays(bases: Sequence[int], pitches: Sequence[int]):
+    return _arr(c_vp, list(bases)), _arr(c_ll, list(pitches))
 
 
 class Batch:

@@ -1,0 +1,70 @@
+"""the paper's GPU design (the reference's own emitted CUDA,
+compiled for sm_100a, oracle/_ref/<prog>_cuda.so) timed beside the fused
+kernel on the same B200, same inputs, same N; one JSON line per program.
+
+Run on a GPU box:  PYTHONPATH=. python scripts/compare_reference_design.py
+"""
+
+import json
+import statistics
+import sys
+
+import torch
+
+from oracle import refcuda
+from oracle.numpy_eval import max_rel_error
+from paper_1804_10120_b200 import bench as tb
+from paper_1804_10120_b200 import eval_program
+from paper_1804_10120_b200.evaluator import plan_for
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 4_000_000  # < 65535*64 (wrapper guard)
+flush = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+
+
+def timed(fn, reps=21):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3)
+    return statistics.median(ts[1:])
+
+
+for name in ("c1_dtg", "c2_maxwell", "c3_christoffel", "p2", "p3"):
+    if not refcuda.available(name):
+        print(json.dumps({"program": name, "skipped": "oracle/_ref not built"}))
+        continue
+    prog, vs = tb.load(tb.PROGRAMS[name])
+    targets = {v.stmt.lhs.field for v in vs}
+    env = tb.make_env(prog, "__none__", 0, tb.DEFAULT_SEED)
+    for f in env.values():
+        f.resize(N)
+        if f.name not in targets:
+            f.data.uniform_()
+    ref_env = {k: (torch.zeros_like(f.data) if k in targets else f.data) for k, f in env.items()}
+    ref = refcuda.RefCudaProgram(name)
+    ref.bind(ref_env)
+    plan = plan_for(vs, env)
+    t_ours = timed(lambda: eval_program(vs, env))
+    t_ref = timed(ref.run)
+    errs = {}
+    bitwise = True
+    for t in targets:
+        a = env[t].data.cpu().numpy()
+        b = ref_env[t].cpu().numpy()
+        errs[t] = max_rel_error(a, b)
+        bitwise &= bool((a.view("u8") == b.view("u8")).all())
+    bytes_ = plan.bytes_per_point * N
+    print(json.dumps({
+        "program": name, "N": N, "bytes_per_point": plan.bytes_per_point,
+        "fused_ms": t_ours * 1e3, "fused_gbs": bytes_ / t_ours / 1e9,
+        "reference_design_ms": t_ref * 1e3, "reference_design_gbs": bytes_ / t_ref / 1e9,
+        "speedup": t_ref / t_ours, "reference_design_launches": len(ref.order),
+        "max_rel_diff": errs, "bitwise_equal": bitwise,
+    }), flush=True)

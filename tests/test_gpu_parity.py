@@ -221,3 +221,31 @@ def test_reference_harness_drives_the_gpu_kernels(case, tmp_path):
     got, want = read_host(out), golden_io(case)[1]
     for t in spec["targets"]:
         assert same_bits(got[t], want[t]), t
+
+
+def test_bound_launch_fast_path_tracks_storage():
+    case = manifest()["cases"]["c1_dtg"]
+    prog, (v,) = program(case["source"])
+    host, want = golden_io("c1_dtg")
+    env = device_env(prog, host)
+    eval_statement(v, env)
+    eval_statement(v, env)  # fast path (bound launch)
+    _check(case, env_to_host(env), want)
+    # new input values in place: same storage, the bound launch sees them
+    env["K"].data.mul_(2.0)
+    eval_statement(v, env)
+    h = env_to_host(env)
+    ref = {k: a.copy() for k, a in h.items()}
+    numpy_eval.eval_statement(v, ref)
+    assert same_bits(h["dtg"], ref["dtg"])
+    # replaced storage and resized target: the fast path must miss
+    env["db"].data = env["db"].data.clone() + 1.0
+    env["dtg"].resize(5)
+    eval_statement(v, env)
+    h = env_to_host(env)
+    ref = {k: a.copy() for k, a in h.items()}
+    numpy_eval.eval_statement(v, ref)
+    assert env["dtg"].gridsize == case["N"] and same_bits(h["dtg"], ref["dtg"])
+    del env["alpha"]
+    with pytest.raises(EvalError, match="'alpha'"):
+        eval_statement(v, env)
