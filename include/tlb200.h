@@ -95,8 +95,9 @@ int tlb_kernel_attrs(tlb_kernel* k, const char* entry, int* regs, int* local_byt
 /* One fused launch over points [0, n) of one grid.  field_bases[f] is the
  * device address of component 0 of field f, components `pitches[f]` doubles
  * apart.  vec: 0 = choose (2-point 128-bit path when every slot is 16-byte
- * aligned), 1 or 2 = force.  threads: block size (0 = 256).  max_blocks:
- * grid cap (0 = one full wave at occupancy).  Asynchronous on `stream`. */
+ * aligned), 1 or 2 = force.  threads: block size (0 = 256; must not exceed
+ * the TLK_THREADS the kernel was compiled with).  max_blocks: grid cap
+ * (0 = one full wave at occupancy, -w = w waves).  Asynchronous on `stream`. */
 int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
                const long long* pitches, int vec, int threads, long long max_blocks,
                void* stream);

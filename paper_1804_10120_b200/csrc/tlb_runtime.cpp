@@ -457,14 +457,14 @@ int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n, const uint6
   long long units = vec2 ? n / 2 : n;
   if (units < 1) units = 1;
   long long blocks = (units + threads - 1) / threads;
-  long long cap = max_blocks > 0 ? max_blocks
-                                 : (long long)st->sm_count * L->occ[e] *
-                                       (threads == kDefaultThreads ? 1 : 1);
-  if (max_blocks <= 0 && threads != kDefaultThreads) {
-    int occ = 0;
+  // max_blocks > 0: explicit cap; 0: one full wave at occupancy; -w: w waves
+  int occ = L->occ[e];
+  if (threads != kDefaultThreads) {
     g_cu.OccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn[e], threads, 0);
-    cap = (long long)st->sm_count * std::max(occ, 1);
+    occ = std::max(occ, 1);
   }
+  long long waves = max_blocks < 0 ? -max_blocks : 1;
+  long long cap = max_blocks > 0 ? max_blocks : (long long)st->sm_count * occ * waves;
   blocks = std::max(1LL, std::min(blocks, cap));
   void* args[] = {param.data()};
   CU(g_cu.LaunchKernel(L->fn[e], (unsigned)blocks, 1, 1, (unsigned)threads, 1, 1, 0, stream,

@@ -33,6 +33,14 @@
 #ifndef TLK_THREADS
 #define TLK_THREADS 256
 #endif
+// Unroll factor of the grid-stride loops (1 = one point group per trip; the
+// per-point body already exposes all of its loads, occupancy does the rest).
+#ifndef TLK_UNROLL
+#define TLK_UNROLL 1
+#endif
+#define TLK_STR2(x) #x
+#define TLK_STR(x) TLK_STR2(x)
+#define TLK_LOOP _Pragma(TLK_STR(unroll TLK_UNROLL))
 
 // ----------------------------------------------------------- lane arithmetic
 __device__ __forceinline__ double2 operator+(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -123,6 +131,7 @@ struct tlk_shared_ptrs {
 extern "C" __global__ void __launch_bounds__(TLK_THREADS)
 tlk_flat_v1(const tlk_flat_params prm) {
   const long long stride = (long long)gridDim.x * blockDim.x;
+  TLK_LOOP
   for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < prm.n; x += stride)
     tlk_point<double>(prm, x);
 }
@@ -131,6 +140,7 @@ extern "C" __global__ void __launch_bounds__(TLK_THREADS)
 tlk_flat_v2(const tlk_flat_params prm) {
   const long long pairs = prm.n >> 1;
   const long long stride = (long long)gridDim.x * blockDim.x;
+  TLK_LOOP
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride)
     tlk_point<double2>(prm, i << 1);
   if ((prm.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) tlk_point<double>(prm, prm.n - 1);
@@ -151,10 +161,12 @@ __device__ __forceinline__ void tlk_batch_body(const long long* __restrict__ tab
     const tlk_shared_ptrs P{sp};
     if constexpr (sizeof(T) == 16) {
       const long long pairs = n >> 1;
+      TLK_LOOP
       for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride)
         tlk_point<T>(P, i << 1);
       if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) tlk_point<double>(P, n - 1);
     } else {
+      TLK_LOOP
       for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += stride)
         tlk_point<double>(P, x);
     }

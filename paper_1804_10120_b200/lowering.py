@@ -354,15 +354,39 @@ def _operand(x) -> str:
     return x.c_text() if isinstance(x, _Lit) else f"v{x}"
 
 
-def _emit_body(instrs: list[Instr], hoist_loads: bool = False) -> list[str]:
+def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = False,
+               restrict: bool = True) -> list[str]:
+    """C++ text of the per-point body.
+
+    With ``restrict`` (default) the body is a function of one
+    ``__restrict__`` pointer per slot: distinct (field, component) slots
+    never overlap (components of a field are ``pitch >= n`` apart, fields
+    are distinct allocations, aliased names were merged into one field), so
+    the compiler may issue every load as early as register pressure allows
+    instead of keeping each load behind the preceding stores.  Loads of a
+    slot only ever precede its stores (the register shadow serves reads
+    after writes), so no load may legally move *after* a store of its own
+    slot, and none is asked to.  ``hoist_loads`` additionally places all
+    loads first in the source.
+    """
     # keep only the final store of every slot; earlier values were consumed
     # through the register shadow
     last = {}
     for k, ins in enumerate(instrs):
         if ins.op == "st":
             last[ins.slot] = k
-    out = ["template <typename T, typename P>",
-           "__device__ __forceinline__ void tlk_point(const P& P_, const long long x) {"]
+    nslots = len(slot_flags)
+    if restrict:
+        params = ", ".join(
+            ("double* __restrict__" if slot_flags[j] & SLOT_WRITE else
+             "const double* __restrict__") + f" p{j}" for j in range(nslots))
+        out = ["template <typename T>",
+               f"__device__ __forceinline__ void tlk_body(const long long x, {params}) {{"]
+        ptr = "p{}".format
+    else:
+        out = ["template <typename T, typename P>",
+               "__device__ __forceinline__ void tlk_point(const P& P_, const long long x) {"]
+        ptr = "P_.p[{}]".format
     if hoist_loads:
         # SSA + one load per slot before any store of that slot: loads may
         # all be issued first (maximum memory-level parallelism)
@@ -370,13 +394,13 @@ def _emit_body(instrs: list[Instr], hoist_loads: bool = False) -> list[str]:
         last = {ins.slot: k for k, ins in enumerate(instrs) if ins.op == "st"}
     for k, ins in enumerate(instrs):
         if ins.op == "ld":
-            out.append(f"  const T v{ins.dst} = tl_ld<T>(P_.p[{ins.slot}] + x);")
+            out.append(f"  const T v{ins.dst} = tl_ld<T>({ptr(ins.slot)} + x);")
         elif ins.op == "st":
             if last[ins.slot] != k:
                 continue
             val = ins.a
             src = f"tl_splat<T>{val.c_text()}" if isinstance(val, _Lit) else f"v{val}"
-            out.append(f"  tl_st(P_.p[{ins.slot}] + x, {src});")
+            out.append(f"  tl_st({ptr(ins.slot)} + x, {src});")
         elif ins.op in _CSYM:
             out.append(f"  const T v{ins.dst} = {_operand(ins.a)} {_CSYM[ins.op]} "
                        f"{_operand(ins.b)};")
@@ -387,6 +411,11 @@ def _emit_body(instrs: list[Instr], hoist_loads: bool = False) -> list[str]:
         else:  # pragma: no cover
             raise LoweringError(f"bad instruction {ins}")
     out.append("}")
+    if restrict:
+        args = ", ".join(f"P_.p[{j}]" for j in range(nslots))
+        out += ["template <typename T, typename P>",
+                "__device__ __forceinline__ void tlk_point(const P& P_, const long long x) {",
+                f"  tlk_body<T>(x, {args});", "}"]
     return out
 
 
@@ -401,7 +430,7 @@ def template_text() -> str:
 
 def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = None,
                   components: Sequence[set[int] | None] | None = None,
-                  hoist_loads: bool = False) -> KernelPlan:
+                  hoist_loads: bool | None = None) -> KernelPlan:
     """Lower validated statements, executed in order per grid point, to one
     fused kernel.  ``alias`` maps field names to a representative name when
     several names address the same storage.  ``components`` optionally
@@ -409,6 +438,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     per-component "Arrays" pathway, evaluator.py:239-257)."""
     if not statements:
         raise LoweringError("nothing to lower: no statements")
+    if hoist_loads is None:
+        hoist_loads = os.environ.get("TLK_HOIST", "0") == "1"
     low = _Lowerer(alias)
     lhs_fields = []
     for k, v in enumerate(statements):
@@ -425,7 +456,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     slot_comp = [0] * n_slots
     for (f, c), s in b.slots.items():
         slot_field[s], slot_comp[s] = f, c
-    body = "\n".join(_emit_body(b.instrs, hoist_loads))
+    restrict = os.environ.get("TLK_RESTRICT", "1") == "1"
+    body = "\n".join(_emit_body(b.instrs, b.slot_flags, hoist_loads, restrict))
     header = [f"// generated by paper_1804_10120_b200.lowering ({LOWERING_VERSION})"]
     for v in statements:
         header.append("// " + _statement_comment(v))

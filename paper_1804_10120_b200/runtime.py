@@ -110,6 +110,15 @@ def nvrtc_version() -> tuple[int, int]:
     return a.value, b.value
 
 
+def launch_config() -> tuple[int, int]:
+    """(threads per block, grid cap) for launches: TLK_THREADS (default 256,
+    also the kernels' __launch_bounds__) and TLK_WAVES (0 = one full wave at
+    occupancy, w > 0 = w waves) — tuning knobs, see scripts/tune_kernel.py."""
+    threads = int(os.environ.get("TLK_THREADS", "256"))
+    waves = int(os.environ.get("TLK_WAVES", "0"))
+    return threads, (-waves if waves > 0 else 0)
+
+
 def compile_options() -> list[str]:
     opts = list(BASE_OPTIONS)
     threads = int(os.environ.get("TLK_THREADS", "256"))
@@ -157,6 +166,8 @@ class Kernel:
                                      _arr(c_int, plan.slot_flags)), "tlb_kernel_set_slots")
         self.nfields = len(plan.fields)
         self.launches = 0
+        self.threads, self.max_blocks = launch_config()
+        self.vec = int(os.environ.get("TLK_VEC", "0"))  # 0 auto, 1 or 2 forced
 
     @property
     def log(self) -> str:
@@ -174,14 +185,19 @@ class Kernel:
         return {"registers": r.value, "local_bytes": lb.value, "max_threads": mt.value}
 
     def launch(self, n: int, bases: Sequence[int], pitches: Sequence[int], stream: int,
-               vec: int = 0, threads: int = 0, max_blocks: int = 0) -> None:
+               vec: int | None = None, threads: int | None = None,
+               max_blocks: int | None = None) -> None:
+        vec = self.vec if vec is None else vec
+        threads = self.threads if threads is None else threads
+        max_blocks = self.max_blocks if max_blocks is None else max_blocks
         check(lib().tlb_launch(self.handle, n, _arr(c_vp, bases), _arr(c_ll, pitches), vec,
                                threads, max_blocks, stream), "tlb_launch")
         self.launches += 1
 
     def launch_arrays(self, n: int, bases, pitches, stream: int) -> None:
         """Launch with prebuilt ctypes address arrays (bound-launch fast path)."""
-        rc = _lib.tlb_launch(self.handle, n, bases, pitches, 0, 0, 0, stream)
+        rc = _lib.tlb_launch(self.handle, n, bases, pitches, self.vec, self.threads,
+                             self.max_blocks, stream)
         if rc:
             check(rc, "tlb_launch")
         self.launches += 1
@@ -214,7 +230,8 @@ class Batch:
         self.handle = h
         self.ndom = len(ns)
 
-    def launch(self, stream: int, threads: int = 0) -> None:
+    def launch(self, stream: int, threads: int | None = None) -> None:
+        threads = self.kernel.threads if threads is None else threads
         check(lib().tlb_batch_launch(self.handle, threads, stream), "tlb_batch_launch")
         self.kernel.launches += 1
 

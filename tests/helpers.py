@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import json
+import random
 from functools import lru_cache
 from pathlib import Path
 
@@ -166,3 +167,52 @@ def random_host_env(prog, n: int, seed: int) -> dict:
     for name in prog.decls.scalar_fields:
         out[name] = rng.uniform(0.0, 1.0, n)
     return out
+
+
+FUZZ_DECLS = ("tensor A dim 3 rank 1;\ntensor B dim 3 rank 2;\ntensor S dim 3 rank 2 sym(0,1);\n"
+         "tensor D dim 3 rank 2 sym(0,1) inner rank 1;\ntensor Q dim 4 rank 2 sym(0,1);\n"
+         "tensor R dim 4 rank 3 sym(1,2);\nfield w;\nconst cc = 1.5;\nindex p: 2;\n")
+
+LEAVES = {
+    "i": ["A(i)", "B(i, 1)", "S(0, i)", "D(i, i)(0)", "Sum(j, B(i, j)*A(j))",
+          "Sum(k, D(i, k)(k))", "A(p+1)*0 + A(i)", "B(i, p)*0 + A(i)"],
+    "ij": ["B(i, j)", "B(j, i)", "S(i, j)", "S(j, i)", "A(i)*A(j)", "Sum(k, B(i, k)*S(k, j))",
+           "D(i, j)(0)", "Sum(k, D(j, i)(k)*A(k))", "B(i+0, j)"],
+    "ijk": ["D(i, j)(k)", "D(j, k)(i)", "A(i)*B(j, k)", "Sum(l, D(i, l)(k)*B(l, j))"],
+    "ab": ["Q(a, b)", "Q(b, a)", "Sum(c, Q(a, c)*Q(c, b))", "R(0, a, b)", "R(a, b, 3)"],
+    "abc": ["R(a, b, c)", "R(a, c, b)", "Q(a, b)*Q(c, 0)", "Sum(d, R(a, d, b)*Q(d, c))"],
+}
+LHS = [("A(i)", "i"), ("B(i, j)", "ij"), ("S(sym<0,1>, i, j)", "ij"), ("B(i, 0)", "i"),
+       ("D(i, j)(k)", "ijk"), ("Q(sym<0,1>, a, b)", "ab"), ("R(a, sym<1,2>, b, c)", "abc"),
+       ("R(sym<1,2>, a, b, c)", "abc"), ("S(i, j)", "ij"), ("B(i, i)", "i")]
+SCALARS = ["w", "cc", "2", "0.25", "sqrt(w)", "(w + 1)", "Sum(i, A(i))", "S(0, 1)", "Q(0, 3)",
+           "-w", "(w*w - cc)"]
+
+
+def fuzz_statement(rng: random.Random) -> str:
+    """One random statement over FUZZ_DECLS (mostly valid, some not)."""
+    def scal(d):
+        if d == 0 or rng.random() < 0.5:
+            return rng.choice(SCALARS)
+        return f"({scal(d - 1)} {rng.choice('+-*/')} {scal(d - 1)})"
+
+    def vec(free, d):
+        if d == 0 or rng.random() < 0.35:
+            return rng.choice(LEAVES[free])
+        r = rng.random()
+        if r < 0.3:
+            return f"({vec(free, d - 1)} {rng.choice('+-')} {vec(free, d - 1)})"
+        if r < 0.5:
+            return f"{scal(1)}*{vec(free, d - 1)}"
+        if r < 0.65:
+            return f"{vec(free, d - 1)}/{scal(1)}"
+        if r < 0.8:
+            return f"-{vec(free, d - 1)}"
+        return f"{vec(free, d - 1)}*{scal(1)}"
+
+    lhs, free = rng.choice(LHS)
+    op = rng.choice(["=", "=", "+=", "-=", "*=", "/="])
+    rhs = scal(2) if op in ("*=", "/=") or rng.random() < 0.05 else vec(free, 3)
+    if rng.random() < 0.05:  # an occasional invalid mutation
+        rhs = rhs.replace("(i", "(z", 1).replace("(a", "(i", 1)
+    return f"{lhs} {op} {rhs};\n"

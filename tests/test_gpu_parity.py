@@ -249,3 +249,36 @@ def test_bound_launch_fast_path_tracks_storage():
     del env["alpha"]
     with pytest.raises(EvalError, match="'alpha'"):
         eval_statement(v, env)
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_fuzzed_programs_match_oracle(seed):
+    # random valid statements over dims 3 and 4, symmetric/nested/inner
+    # groups, offsets, fixed slots, literals, sqrt/division, op=; fused
+    # into one kernel and checked bitwise against the oracle
+    import random
+
+    from helpers import FUZZ_DECLS, fuzz_statement
+    from paper_1804_10120_b200.ir import ValidationError, validate_statement
+    from paper_1804_10120_b200.parser import parse_program
+
+    rng = random.Random(1000 + seed)
+    stmts = []
+    while len(stmts) < 1 + seed % 4:
+        res = parse_program(FUZZ_DECLS + fuzz_statement(rng))
+        if not res.ok:
+            continue
+        try:
+            stmts.append(validate_statement(res.program.statements[0], res.program.decls))
+        except ValidationError:
+            continue
+    prog = parse_program(FUZZ_DECLS).program
+    n = [1, 2, 7, 64, 255, 1000][seed % 6]
+    host = random_host_env(prog, n, seed)
+    want = {k: a.copy() for k, a in host.items()}
+    numpy_eval.eval_program(stmts, want)
+    env = device_env(prog, host)
+    eval_program(stmts, env)
+    got = env_to_host(env)
+    for k in want:
+        assert same_bits(got[k], want[k]), (k, [str(v.stmt) for v in stmts])
