@@ -65,7 +65,8 @@ template <> __device__ __forceinline__ double2 tl_splat<double2>(double c) { ret
 
 // ------------------------------------------------------------ memory access
 // TLK_LDMODE 0: ld.global.cs (streaming)            [default]
-//            1: ld.global.nc.L1::no_allocate (read-only path, no L1 fill)
+//            1: ld.global.nc.L1::no_allocate as a movable asm (the lowering
+//               only selects it when no slot is both read and written)
 //            2: plain ld.global
 #ifndef TLK_LDMODE
 #define TLK_LDMODE 0

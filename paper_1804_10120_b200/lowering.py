@@ -155,6 +155,8 @@ class KernelPlan:
     statements: int
     key: str = ""
     lhs_fields: list[int] = dc_field(default_factory=list)
+    variant: "Variant | None" = None
+    phases: int = 1
 
     @property
     def n_slots(self) -> int:
@@ -187,6 +189,7 @@ class _Builder:
         self.slot_flags: list[int] = []
         self.shadow: dict[int, Any] = {}  # slot -> current operand
         self.flops = 0
+        self.chained = 0  # reads served by the register shadow of a written slot
 
     def slot(self, f: int, c: int) -> int:
         key = (f, c)
@@ -201,6 +204,8 @@ class _Builder:
 
     def read(self, f: int, c: int):
         s = self.slot(f, c)
+        if self.slot_flags[s] & SLOT_WRITE:
+            self.chained += 1
         if s not in self.shadow:
             r = self.reg()
             self.instrs.append(Instr("ld", r, slot=s))
@@ -428,18 +433,88 @@ def template_text() -> str:
     return _TEMPLATE_CACHE[0]
 
 
+@dataclass(frozen=True)
+class Variant:
+    """Code-generation and launch choices of one fused kernel.
+
+    restrict  per-slot ``__restrict__`` body parameters (always legal: slots
+              never overlap)
+    hoist     every load first in the body source
+    ldmode    0 ``ld.global.cs``; 1 ``ld.global.nc.L1::no_allocate`` as a
+              side-effect-free asm the compiler may move freely — only legal
+              when no slot is both read and written (a load could otherwise
+              sink below a later store of its own slot), enforced here
+    vec       2 = two points per thread step (128-bit accesses), 1 = one
+    waves     grid = waves x SMs x resident blocks (grid-stride loop)
+    """
+
+    restrict: bool = True
+    hoist: bool = False
+    ldmode: int = 0
+    vec: int = 2
+    waves: int = 1
+
+    def tag(self) -> str:
+        return (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
+                f"v{self.vec}w{self.waves}")
+
+
+def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
+                   chained: int) -> Variant:
+    """Default per-kernel choice — a policy fitted to measurements on B200
+    (profiles/r01/tune_*.jsonl: 12 variants x 8 programs at 2^24-2^26 points).
+
+    * light kernels (at most ~1.5 arithmetic ops per streamed array: C1,
+      Maxwell, K_ij) are pure streams: one point per thread (8-byte
+      accesses, twice the threads in flight) over 4 waves of blocks —
+      +5-7 % over the 2-point variant;
+    * heavier kernels keep 2 points per thread (128-bit accesses).  When no
+      slot is both read and written, loads are made freely movable (the
+      compiler schedules them against register pressure instead of behind
+      earlier stores: +2 % on P2, +8 % on the write-heavy outer products);
+      when statements also chain through registers (P3: Γ → ∇β → ∂t g)
+      every load is hoisted to the top, otherwise each statement's loads
+      wait for the previous statement's stores (2.1x on P3);
+    * with read-modify-write slots the restrict-free 2-point body over 4
+      waves is used.
+    """
+    arrays = reads + writes
+    if n_ops <= 1.5 * arrays:
+        return Variant(restrict=True, hoist=False, ldmode=0, vec=1, waves=4)
+    if rw_slots == 0:
+        return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=2, waves=4 if chained else 1)
+    return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
+
+
+def _env_variant(v: Variant) -> Variant:
+    """TLK_* environment overrides (tuning experiments, scripts/tune_kernel.py)."""
+    env = os.environ
+    kw = {}
+    if "TLK_RESTRICT" in env:
+        kw["restrict"] = env["TLK_RESTRICT"] == "1"
+    if "TLK_HOIST" in env:
+        kw["hoist"] = env["TLK_HOIST"] == "1"
+    if "TLK_LDMODE" in env:
+        kw["ldmode"] = int(env["TLK_LDMODE"])
+    if "TLK_VEC" in env:
+        kw["vec"] = int(env["TLK_VEC"])
+    if "TLK_WAVES" in env:
+        kw["waves"] = int(env["TLK_WAVES"])
+    return Variant(**{**v.__dict__, **kw}) if kw else v
+
+
 def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = None,
                   components: Sequence[set[int] | None] | None = None,
-                  hoist_loads: bool | None = None) -> KernelPlan:
+                  hoist_loads: bool | None = None, variant: Variant | None = None) -> KernelPlan:
     """Lower validated statements, executed in order per grid point, to one
     fused kernel.  ``alias`` maps field names to a representative name when
     several names address the same storage.  ``components`` optionally
     restricts statement k to the given LHS component ordinals (the paper's
-    per-component "Arrays" pathway, evaluator.py:239-257)."""
+    per-component "Arrays" pathway, evaluator.py:239-257).  ``variant``
+    fixes the code-generation/launch choices (default: ``choose_variant``,
+    then TLK_* environment overrides)."""
     if not statements:
         raise LoweringError("nothing to lower: no statements")
-    if hoist_loads is None:
-        hoist_loads = os.environ.get("TLK_HOIST", "0") == "1"
     low = _Lowerer(alias)
     lhs_fields = []
     for k, v in enumerate(statements):
@@ -456,21 +531,45 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     slot_comp = [0] * n_slots
     for (f, c), s in b.slots.items():
         slot_field[s], slot_comp[s] = f, c
-    restrict = os.environ.get("TLK_RESTRICT", "1") == "1"
-    body = "\n".join(_emit_body(b.instrs, b.slot_flags, hoist_loads, restrict))
-    header = [f"// generated by paper_1804_10120_b200.lowering ({LOWERING_VERSION})"]
+    n_ops = sum(1 for i in b.instrs if i.op not in ("ld", "st"))
+    reads = sum(1 for f in b.slot_flags if f & SLOT_READ)
+    writes = sum(1 for f in b.slot_flags if f & SLOT_WRITE)
+    rw = sum(1 for f in b.slot_flags if f == SLOT_READ | SLOT_WRITE)
+    phases = _phases(b.instrs)
+    if variant is None:
+        variant = _env_variant(choose_variant(reads, writes, n_ops, rw, b.chained))
+    if hoist_loads is not None:
+        variant = Variant(**{**variant.__dict__, "hoist": hoist_loads})
+    if variant.ldmode == 1 and rw:
+        variant = Variant(**{**variant.__dict__, "ldmode": 0})  # see Variant docstring
+    body = "\n".join(_emit_body(b.instrs, b.slot_flags, variant.hoist, variant.restrict))
+    header = [f"// generated by paper_1804_10120_b200.lowering ({LOWERING_VERSION})",
+              f"// variant {variant.tag()}"]
     for v in statements:
         header.append("// " + _statement_comment(v))
     header.append(f"#define TLK_NSLOTS {n_slots}")
+    header.append(f"#define TLK_LDMODE {variant.ldmode}")
     src = "\n".join(header) + "\n" + template_text().replace("// @@TLK_BODY@@", body)
-    n_ops = sum(1 for i in b.instrs if i.op not in ("ld", "st"))
     plan = KernelPlan(src, low.fields, slot_field, slot_comp, list(b.slot_flags), b.flops, n_ops,
-                      len(statements), lhs_fields=lhs_fields)
+                      len(statements), lhs_fields=lhs_fields, variant=variant, phases=phases)
     # identical source text can serve different slot maps (e.g. the
     # per-component kernels of one statement): the plan identity covers both
-    ident = f"{src}\0{slot_field}\0{slot_comp}\0{plan.slot_flags}"
+    ident = f"{src}\0{slot_field}\0{slot_comp}\0{plan.slot_flags}\0{variant.tag()}"
     plan.key = hashlib.sha256(ident.encode()).hexdigest()
     return plan
+
+
+def _phases(instrs: list[Instr]) -> int:
+    """Number of load groups separated by stores in program order (1 = all
+    loads precede all stores)."""
+    n, seen_store = 0, True
+    for ins in instrs:
+        if ins.op == "st":
+            seen_store = True
+        elif ins.op == "ld" and seen_store:
+            n += 1
+            seen_store = False
+    return n
 
 
 def _statement_comment(v) -> str:

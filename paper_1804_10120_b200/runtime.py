@@ -112,11 +112,10 @@ def nvrtc_version() -> tuple[int, int]:
 
 def launch_config() -> tuple[int, int]:
     """(threads per block, grid cap) for launches: TLK_THREADS (default 256,
-    also the kernels' __launch_bounds__) and TLK_WAVES (0 = one full wave at
-    occupancy, w > 0 = w waves) — tuning knobs, see scripts/tune_kernel.py."""
+    also the kernels' __launch_bounds__); the number of waves comes from the
+    plan's Variant (lowering.choose_variant / TLK_WAVES)."""
     threads = int(os.environ.get("TLK_THREADS", "256"))
-    waves = int(os.environ.get("TLK_WAVES", "0"))
-    return threads, (-waves if waves > 0 else 0)
+    return threads, 0
 
 
 def compile_options() -> list[str]:
@@ -167,7 +166,11 @@ class Kernel:
         self.nfields = len(plan.fields)
         self.launches = 0
         self.threads, self.max_blocks = launch_config()
-        self.vec = int(os.environ.get("TLK_VEC", "0"))  # 0 auto, 1 or 2 forced
+        var = plan.variant
+        # vec 2 = auto (128-bit when every slot is 16-byte aligned), 1 = forced scalar
+        self.vec = 1 if (var is not None and var.vec == 1) else 0
+        if var is not None and var.waves > 1 and self.max_blocks == 0:
+            self.max_blocks = -var.waves
 
     @property
     def log(self) -> str:

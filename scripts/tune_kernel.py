@@ -19,14 +19,15 @@ POINTS = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 26
 VARIANTS = {
     "base": {},
     "norestrict": {"TLK_RESTRICT": "0"},
-    "hoist": {"TLK_HOIST": "1"},
     "vec1": {"TLK_VEC": "1"},
-    "hoist_vec1": {"TLK_HOIST": "1", "TLK_VEC": "1"},
-    "hoist_t128": {"TLK_HOIST": "1", "TLK_THREADS": "128"},
-    "hoist_vec1_t128": {"TLK_HOIST": "1", "TLK_VEC": "1", "TLK_THREADS": "128"},
-    "unroll4": {"TLK_DEFINES": "-DTLK_UNROLL=4"},
+    "vec1_norestrict": {"TLK_VEC": "1", "TLK_RESTRICT": "0"},
+    "vec1_waves4": {"TLK_VEC": "1", "TLK_WAVES": "4"},
+    "norestrict_waves4": {"TLK_RESTRICT": "0", "TLK_WAVES": "4"},
+    "ldnc": {"TLK_DEFINES": "-DTLK_LDMODE=1"},
+    "ldnc_vec1": {"TLK_DEFINES": "-DTLK_LDMODE=1", "TLK_VEC": "1"},
     "hoist_ldnc": {"TLK_HOIST": "1", "TLK_DEFINES": "-DTLK_LDMODE=1"},
-    "hoist_stplain": {"TLK_HOIST": "1", "TLK_DEFINES": "-DTLK_STMODE=1"},
+    "hoist_ldnc_vec1": {"TLK_HOIST": "1", "TLK_DEFINES": "-DTLK_LDMODE=1", "TLK_VEC": "1"},
+    "hoist_ldnc_waves4": {"TLK_HOIST": "1", "TLK_DEFINES": "-DTLK_LDMODE=1", "TLK_WAVES": "4"},
     "hoist_waves4": {"TLK_HOIST": "1", "TLK_WAVES": "4"},
 }
 
@@ -35,8 +36,13 @@ import json, os, statistics, sys, torch
 from paper_1804_10120_b200 import bench as tb, eval_program
 from paper_1804_10120_b200.evaluator import plan_for, kernel_for
 n = int(sys.argv[1])
-for name in ("p2", "c3_christoffel", "c1_dtg", "c2_maxwell", "p3"):
-    prog, vs = tb.load(tb.PROGRAMS[name])
+suite = {e.name: e.source for e in tb.builtin_suite()}
+progs = dict(tb.PROGRAMS)
+progs.update({"contract1": suite["contract1"], "outer3": suite["outer3"], "kij": suite["kij"]})
+n0 = n
+for name in ("p2", "c3_christoffel", "c1_dtg", "c2_maxwell", "p3", "contract1", "outer3", "kij"):
+    n = n0 // 4 if name in ("contract1", "outer3") else n0
+    prog, vs = tb.load(progs[name])
     targets = {v.stmt.lhs.field for v in vs}
     env = tb.make_env(prog, "__none__", 0, tb.DEFAULT_SEED)
     for f in env.values():
@@ -54,7 +60,7 @@ for name in ("p2", "c3_christoffel", "c1_dtg", "c2_maxwell", "p3"):
         ts.append(a.elapsed_time(b) / 1e3)
     t = statistics.median(ts[1:])
     k = kernel_for(vs, env)
-    print(json.dumps({"program": name, "t_ms": t * 1e3,
+    print(json.dumps({"program": name, "t_ms": t * 1e3, "n": n,
                       "gbs": plan.bytes_per_point * n / t / 1e9,
                       "regs": k.attrs("tlk_flat_v2")["registers"]}), flush=True)
     del env

@@ -282,3 +282,31 @@ def test_fuzzed_programs_match_oracle(seed):
     got = env_to_host(env)
     for k in want:
         assert same_bits(got[k], want[k]), (k, [str(v.stmt) for v in stmts])
+
+
+VARIANTS = [dict(restrict=False), dict(hoist=True), dict(vec=1), dict(ldmode=1),
+            dict(hoist=True, ldmode=1, vec=1), dict(waves=4)]
+
+
+@pytest.mark.parametrize("vkw", VARIANTS, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()))
+@pytest.mark.parametrize("name", CASES)
+def test_every_codegen_variant_is_bit_exact(name, vkw):
+    from paper_1804_10120_b200.lowering import Variant, lower_program
+    from paper_1804_10120_b200.runtime import Kernel
+
+    case = manifest()["cases"][name]
+    prog, vs = program(case["source"])
+    host, want = golden_io(name)
+    env = device_env(prog, host)
+    from paper_1804_10120_b200.evaluator import _bind, _prepare
+
+    sizes = {_prepare(v, env)[1] for v in vs}
+    if len(sizes) != 1:
+        pytest.skip("program is not fusable (sizes differ)")
+    n = sizes.pop()
+    _, _, stores = _bind(vs, env)
+    plan = lower_program(vs, variant=Variant(**vkw))
+    k = Kernel(plan)
+    k.launch(n, [s.base for s in stores], [s.pitch for s in stores],
+             torch.cuda.current_stream().cuda_stream)
+    _check(case, env_to_host(env), want)

@@ -112,3 +112,24 @@ def test_same_source_different_slot_maps_are_distinct_kernels():
     assert p1.source == p2.source and p1.key != p2.key
     assert get_kernel(p1) is not get_kernel(p2)
     assert get_kernel(p1).cache_key == get_kernel(p2).cache_key  # cubin shared on disk
+
+
+def test_movable_loads_refused_when_a_slot_is_read_and_written():
+    from paper_1804_10120_b200.lowering import Variant
+
+    _, vs = program("tensor A dim 3 rank 1;\ntensor B dim 3 rank 1;\nA(i) += B(i);\n")
+    plan = lower_program(vs, variant=Variant(ldmode=1))
+    assert plan.variant.ldmode == 0 and "#define TLK_LDMODE 0" in plan.source
+    _, vs = program("tensor A dim 3 rank 1;\ntensor B dim 3 rank 1;\nA(i) = B(i);\n")
+    plan = lower_program(vs, variant=Variant(ldmode=1))
+    assert plan.variant.ldmode == 1 and "#define TLK_LDMODE 1" in plan.source
+
+
+@pytest.mark.parametrize("hoist", [False, True])
+@pytest.mark.parametrize("restrict", [False, True])
+def test_variants_compile(hoist, restrict):
+    from paper_1804_10120_b200.lowering import Variant
+
+    _, vs = program(manifest()["cases"]["c4_p3"]["source"])
+    k = get_kernel(lower_program(vs, variant=Variant(restrict=restrict, hoist=hoist, ldmode=1)))
+    assert "DFMA" not in _sass(k)
