@@ -104,10 +104,12 @@ int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
 
 /* Multi-domain batch: ndom subdomains, each with its own field bases
  * (field_bases[d*nfields+f]), pitches and point count ns[d].  The table is
- * resolved to per-slot pointers and uploaded once; tlb_batch_launch is then a
- * single kernel launch (CUDA-graph capturable). */
+ * resolved to per-slot pointers and uploaded once (synchronously, in the
+ * context owning `stream`); tlb_batch_launch is then a single kernel launch
+ * (CUDA-graph capturable). */
 int tlb_batch_create(tlb_kernel* k, int ndom, const void* const* field_bases,
-                     const long long* pitches, const long long* ns, tlb_batch** out);
+                     const long long* pitches, const long long* ns, void* stream,
+                     tlb_batch** out);
 int tlb_batch_launch(tlb_batch* b, int threads, void* stream);
 void tlb_batch_destroy(tlb_batch* b);
 

@@ -497,11 +497,12 @@ int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
 }
 
 int tlb_batch_create(tlb_kernel* k, int ndom, const void* const* field_bases,
-                     const long long* pitches, const long long* ns, tlb_batch** out) {
+                     const long long* pitches, const long long* ns, void* stream,
+                     tlb_batch** out) {
   if (!k || k->slot_field.empty() || ndom < 1) return fail("tlb_batch_create: bad arguments");
   if (ensure(true)) return 1;
   CUcontext ctx;
-  if (bind_context(nullptr, &ctx)) return 1;
+  if (bind_context(stream, &ctx)) return 1;
   const size_t m = k->slot_field.size();
   const int nf = k->nfields;
   // device record per domain: { long long n; double* p[m]; }

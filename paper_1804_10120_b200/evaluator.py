@@ -467,14 +467,14 @@ class _BatchCache:
     def __init__(self) -> None:
         self._d: dict = {}
 
-    def get(self, kern: Kernel, table: tuple) -> Batch:
+    def get(self, kern: Kernel, table: tuple, stream: int) -> Batch:
         key = (id(kern), table)
         b = self._d.get(key)
         if b is None:
             bases = [[t[0] for t in dom[1]] for dom in table]
             pitches = [[t[1] for t in dom[1]] for dom in table]
             ns = [dom[0] for dom in table]
-            b = Batch(kern, bases, pitches, ns)
+            b = Batch(kern, bases, pitches, ns, stream)
             if len(self._d) > 64:
                 self._d.clear()
             self._d[key] = b
@@ -521,7 +521,8 @@ def eval_batch(vs, envs: Sequence[Env]) -> None:
     dev = table[0][2]
     key = tuple((t[0], t[1]) for t in table)
     with torch.cuda.device(dev):
-        _batches.get(kern, key).launch(torch.cuda.current_stream(dev).cuda_stream)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _batches.get(kern, key, stream).launch(stream)
 
 
 def capture_graph(fn, warmup: int = 1):

@@ -81,7 +81,7 @@ def lib() -> ctypes.CDLL:
                 "tlb_launch": (c_int, [c_vp, c_ll, ctypes.POINTER(c_vp), ctypes.POINTER(c_ll),
                                        c_int, c_int, c_ll, c_vp]),
                 "tlb_batch_create": (c_int, [c_vp, c_int, ctypes.POINTER(c_vp),
-                                             ctypes.POINTER(c_ll), ctypes.POINTER(c_ll),
+                                             ctypes.POINTER(c_ll), ctypes.POINTER(c_ll), c_vp,
                                              ctypes.POINTER(c_vp)]),
                 "tlb_batch_launch": (c_int, [c_vp, c_int, c_vp]),
                 "tlb_batch_destroy": (None, [c_vp]),
@@ -222,13 +222,14 @@ class Batch:
     """Uploaded multi-domain table for one kernel (tlb_batch_*)."""
 
     def __init__(self, kernel: Kernel, bases: Sequence[Sequence[int]],
-                 pitches: Sequence[Sequence[int]], ns: Sequence[int]):
+                 pitches: Sequence[Sequence[int]], ns: Sequence[int], stream: int):
         self.kernel = kernel
         flat_b = [b for row in bases for b in row]
         flat_p = [p for row in pitches for p in row]
         h = c_vp()
         check(lib().tlb_batch_create(kernel.handle, len(ns), _arr(c_vp, flat_b),
-                                     _arr(c_ll, flat_p), _arr(c_ll, list(ns)), ctypes.byref(h)),
+                                     _arr(c_ll, flat_p), _arr(c_ll, list(ns)), stream,
+                                     ctypes.byref(h)),
               "tlb_batch_create")
         self.handle = h
         self.ndom = len(ns)
