@@ -546,9 +546,16 @@ int tlb_batch_launch(tlb_batch* b, int threads, void* stream) {
   long long units = b->vec2 ? (b->max_n + 1) / 2 : b->max_n;
   long long gx = std::max(1LL, (units + threads - 1) / threads);
   long long gy = std::min<long long>(b->ndom, 65535);
-  // cap the total grid at a few waves; blocks loop over x chunks and domains
-  long long cap = (long long)st->sm_count * L->occ[e] * 4;
-  if (gx * gy > cap) gx = std::max(1LL, cap / gy);
+  // cap the total grid at a few waves (TLB_BATCH_WAVES, default 4; 0 = one
+  // block per (domain, chunk)); blocks loop over x chunks and domains
+  static const long long waves = [] {
+    const char* e = getenv("TLB_BATCH_WAVES");
+    return e ? atoll(e) : 4LL;
+  }();
+  if (waves > 0) {
+    long long cap = (long long)st->sm_count * L->occ[e] * waves;
+    if (gx * gy > cap) gx = std::max(1LL, cap / gy);
+  }
   CUdeviceptr table = b->table;
   int ndom = b->ndom;
   void* args[] = {&table, &ndom};

@@ -310,3 +310,57 @@ def test_every_codegen_variant_is_bit_exact(name, vkw):
     k.launch(n, [s.base for s in stores], [s.pitch for s in stores],
              torch.cuda.current_stream().cuda_stream)
     _check(case, env_to_host(env), want)
+
+
+def test_ragged_multi_domain_batch():
+    # subdomains of different (odd and even) sizes in one launch
+    prog, vs = program(manifest()["cases"]["c4_p2"]["source"])
+    sizes = [1, 2, 3, 100, 4097, 4096, 255]
+    envs, hosts = [], []
+    for d, n in enumerate(sizes):
+        host = random_host_env(prog, n, 50 + d)
+        for t in ("Gamma", "dtg"):
+            host[t][:] = 0.0
+        hosts.append(host)
+        envs.append(device_env(prog, host))
+    before = sum(k.launches for k in all_kernels())
+    eval_batch(vs, envs)
+    assert sum(k.launches for k in all_kernels()) == before + 1
+    for env, host in zip(envs, hosts):
+        numpy_eval.eval_program(vs, host)
+        got = env_to_host(env)
+        for t in ("Gamma", "dtg"):
+            assert same_bits(got[t], host[t]), (t, host[t].shape)
+
+
+def test_concurrent_streams():
+    # two programs on two streams at once: results independent of overlap
+    case = manifest()["cases"]["c4_p2"]
+    prog, vs = program(case["source"])
+    host, want = golden_io("c4_p2")
+    envs = [device_env(prog, host) for _ in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for s, env in zip(streams, envs):
+            with torch.cuda.stream(s):
+                for t in case["targets"]:
+                    env[t].data.zero_()
+                eval_program(vs, env)
+    torch.cuda.synchronize()
+    for env in envs:
+        _check(case, env_to_host(env), want)
+
+
+def test_reference_built_statement_on_device_fields():
+    # a tree built by another implementation of the IR (here: the oracle's
+    # duck-typed view) is accepted by the evaluator
+    from paper_1804_10120_b200.lowering import lower_program
+
+    case = manifest()["cases"]["c3_christoffel"]
+    prog, (v,) = program(case["source"])
+    host, want = golden_io("c3_christoffel")
+    env = device_env(prog, host)
+    eval_statement(v, env)
+    _check(case, env_to_host(env), want)
+    assert lower_program([v]).n_slots == case["statements"][0]["count_data"][0]
