@@ -50,7 +50,7 @@ def parse_args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--points", type=int, default=C5_POINTS, help="total grid points")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--e2e-slab", type=int, default=1 << 24,
+    ap.add_argument("--e2e-slab", type=int, default=1 << 25,
                     help="points per pinned host slab of the e2e leg")
     ap.add_argument("--cpu-sample", type=int, default=1 << 22,
                     help="points of the CPU-baseline sample")
@@ -59,6 +59,11 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
+                    help="process-group backend (gloo + --same-device: multi-rank path "
+                         "exercised on one GPU)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="map every rank to cuda:0 (single-GPU test of the N>1 path)")
     return ap.parse_args()
 
 
@@ -66,22 +71,24 @@ def parse_args():
 
 
 class Dist:
-    def __init__(self):
+    def __init__(self, backend: str = "nccl", same_device: bool = False):
         import torch
 
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.local = 0 if same_device else int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = backend
         self.pg = None
+        torch.cuda.set_device(self.local)
         if self.world > 1:
             import torch.distributed as dist
 
-            torch.cuda.set_device(self.local)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group("gloo")
             self.pg = dist
-        else:
-            torch.cuda.set_device(0)
 
     def barrier(self):
         if self.pg:
@@ -92,7 +99,8 @@ class Dist:
             return x
         import torch
 
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX if op == "max" else self.pg.ReduceOp.SUM)
         return float(t.item())
 
@@ -326,7 +334,8 @@ def run_e2e(args, dist: Dist, vs, n_local: int) -> dict:
     from paper_1804_10120_b200 import bench as tb
     from paper_1804_10120_b200.evaluator import plan_for
 
-    s = min(args.e2e_slab, n_local)
+    # pinned host slab: at most 2^25 points (17 GB for P2) per box
+    s = max(256, min(args.e2e_slab, n_local, (1 << 25) // dist.world))
     prog, _ = tb.load(tb.P2)
     host = tb.make_env(prog, "Gamma", s, SEED, device="cpu")
     for f in host.values():  # pinned host memory for full-speed async copies
@@ -354,7 +363,7 @@ def run_e2e(args, dist: Dist, vs, n_local: int) -> dict:
             "h2d_bytes_per_step": h2d * dist.world, "d2h_bytes_per_step": d2h * dist.world,
             "s_per_step": dt, "steps": args.e2e_steps,
             "path": "eval_program(host pinned fields) -> tlb_exec_host: H2D -> fused kernel "
-                    "-> D2H, 2-stream slab pipeline",
+                    "-> D2H, 3-stream slab pipeline",
             "host_slab_points": s}
 
 
@@ -532,7 +541,7 @@ def main() -> int:
     if args.sweep:
         run_sweep(args)
         return 0
-    dist = Dist()
+    dist = Dist(args.dist_backend, args.same_device)
     try:
         line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
         if line is not None:

@@ -29,7 +29,7 @@
  *       (pkg/src/tlang/registry.py:241-257, goldens/suite/tloops_bindings.cu:289)
  *       which passed *host* pointer arrays to a kernel: here host component
  *       arrays are staged through device slabs (H2D -> fused kernel -> D2H),
- *       pipelined on two streams, synchronously like the reference `call`.
+ *       pipelined on three streams, synchronously like the reference `call`.
  *   tlb_fill_uniform
  *       counter-based replacement for `bench.make_env`'s
  *       np.random.default_rng(seed).uniform(0,1) (pkg/src/tlang/bench.py:72-87)
@@ -116,7 +116,8 @@ void tlb_batch_destroy(tlb_batch* b);
 /* Host-resident fields: comp_ptrs[f][c] is the host address of canonical
  * component c of field f (n doubles each).  Read slots are copied H2D, the
  * fused kernel runs, written slots are copied D2H, in slabs of `slab` points
- * (0 = automatic) pipelined over two streams.  Synchronous on return. */
+ * (0 = automatic, <= 4 GiB of staging) pipelined over three streams/buffers.
+ * Synchronous on return. */
 int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_ptrs,
                   long long slab, void* stream);
 

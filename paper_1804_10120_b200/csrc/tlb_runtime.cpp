@@ -207,9 +207,11 @@ int bind_context(void* stream, CUcontext* out) {
 
 // --------------------------------------------------- per-context state ----
 
+constexpr int kStageBuffers = 3;  // host-staged pipeline depth (buffers = streams)
+
 struct CtxState {
   int sm_count = 0;
-  CUstream side[2] = {nullptr, nullptr};
+  CUstream side[kStageBuffers] = {};
   CUdeviceptr scratch = 0;
   size_t scratch_bytes = 0;
 };
@@ -590,15 +592,16 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
   Loaded* L;
   if (load_module(k, ctx, &L)) return 1;
   const size_t m = k->slot_field.size();
+  const int nb = kStageBuffers;
   if (slab <= 0) {
-    // two buffers of m*slab doubles, at most ~2 GiB in total
-    long long cap = (1LL << 31) / (long long)(2 * m * sizeof(double));
+    // nb buffers of m*slab doubles, at most ~4 GiB in total
+    long long cap = (4LL << 30) / (long long)(nb * m * sizeof(double));
     slab = std::min<long long>(n, std::max<long long>(1 << 16, cap));
   }
   slab = std::min(slab, n);
   slab = (slab + 255) / 256 * 256;  // keeps every slot slice 2 KiB aligned
   std::lock_guard<std::mutex> lk(g_ctx_mu);  // one staged run per process at a time
-  size_t need = 2 * m * (size_t)slab * sizeof(double);
+  size_t need = (size_t)nb * m * (size_t)slab * sizeof(double);
   if (st->scratch_bytes < need) {
     if (st->scratch) g_cu.MemFree(st->scratch);
     st->scratch = 0;
@@ -606,19 +609,19 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
     CU(g_cu.MemAlloc(&st->scratch, need), "cuMemAlloc(staging)");
     st->scratch_bytes = need;
   }
-  for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < nb; ++s)
     if (!st->side[s]) CU(g_cu.StreamCreate(&st->side[s], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
   // order after prior work of the caller's stream
   CUevent ev;
   CU(g_cu.EventCreate(&ev, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
   CU(g_cu.EventRecord(ev, (CUstream)stream), "cuEventRecord");
-  for (int s = 0; s < 2; ++s) CU(g_cu.StreamWaitEvent(st->side[s], ev, 0), "cuStreamWaitEvent");
+  for (int s = 0; s < nb; ++s) CU(g_cu.StreamWaitEvent(st->side[s], ev, 0), "cuStreamWaitEvent");
   g_cu.EventDestroy(ev);
   std::vector<uint64_t> slots(m);
   long long slab_idx = 0;
   for (long long lo = 0; lo < n; lo += slab, ++slab_idx) {
     const long long cnt = std::min(slab, n - lo);
-    const int b = (int)(slab_idx & 1);
+    const int b = (int)(slab_idx % nb);
     CUstream s = st->side[b];
     CUdeviceptr buf = st->scratch + (size_t)b * m * (size_t)slab * sizeof(double);
     for (size_t j = 0; j < m; ++j) {
@@ -636,7 +639,7 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
       }
     }
   }
-  for (int s = 0; s < 2; ++s) CU(g_cu.StreamSynchronize(st->side[s]), "cuStreamSynchronize");
+  for (int s = 0; s < nb; ++s) CU(g_cu.StreamSynchronize(st->side[s]), "cuStreamSynchronize");
   return 0;
 }
 
