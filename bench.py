@@ -293,7 +293,8 @@ def run_ours(args, dist: Dist) -> dict | None:
                 "generated on the device",
         "config": {
             "workload": "C5: program P2 = Christoffel Gamma^i_jk (18 comps) + dt g_ij "
-                        "(6 comps), one fused kernel, 2^28 points total",
+                        f"(6 comps), one fused kernel, {args.points} points total"
+                        + (" (2^28, BASELINE configs[4])" if args.points == C5_POINTS else ""),
             "program": "p2",
             "points_total": args.points,
             "points_per_gpu": n_local,
@@ -301,7 +302,8 @@ def run_ours(args, dist: Dist) -> dict | None:
             "bytes_per_point": plan.bytes_per_point,
             "flops_per_point": plan.flops_per_point,
             "arrays": {"read": plan.reads, "written": plan.writes},
-            "l2": "working set 137 GB >> 126 MB L2; no flush needed",
+            "l2": f"working set {plan.bytes_per_point * args.points / 1e9:.1f} GB >> 126 MB L2; "
+                  "no flush needed",
         },
         "hbm_gbs": alg_bytes * dist.world / (ms_per_step / 1e3) / 1e9,
         "roofline": {

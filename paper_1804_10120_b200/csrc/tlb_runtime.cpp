@@ -548,11 +548,12 @@ int tlb_batch_launch(tlb_batch* b, int threads, void* stream) {
   long long units = b->vec2 ? (b->max_n + 1) / 2 : b->max_n;
   long long gx = std::max(1LL, (units + threads - 1) / threads);
   long long gy = std::min<long long>(b->ndom, 65535);
-  // cap the total grid at a few waves (TLB_BATCH_WAVES, default 4; 0 = one
-  // block per (domain, chunk)); blocks loop over x chunks and domains
+  // optional cap of the grid at a few waves (TLB_BATCH_WAVES; default 0 =
+  // one block per (domain, chunk): measured 190 us vs 195 us at 4 waves for
+  // C4); capped blocks loop over x chunks and domains
   static const long long waves = [] {
     const char* e = getenv("TLB_BATCH_WAVES");
-    return e ? atoll(e) : 4LL;
+    return e ? atoll(e) : 0LL;
   }();
   if (waves > 0) {
     long long cap = (long long)st->sm_count * L->occ[e] * waves;

@@ -175,7 +175,7 @@ def _prepare(v, env: Env) -> tuple[Any, int]:
 class _Storage:
     """Where one field's numbers are and how its components are laid out."""
 
-    __slots__ = ("where", "device", "base", "pitch", "ncomp", "key", "_offsets")
+    __slots__ = ("where", "device", "base", "pitch", "ncomp", "key", "_offsets", "extent")
 
     def __init__(self, field, ncomp_expected: int, name: str):
         data = field.data
@@ -199,11 +199,14 @@ class _Storage:
             ncomp, oc, ic = 1, 1, 1
             if shape[0] > 1 and strides[0] != 1:
                 raise EvalError(f"field {name!r}: grid dimension must be unit-stride")
+            self.extent = shape[0]  # elements spanned
         else:
             oc, ic, npts = shape
             ncomp = oc * ic
             if npts > 1 and strides[2] != 1:
                 raise EvalError(f"field {name!r}: grid dimension must be unit-stride")
+            self.extent = ((oc - 1) * strides[0] + (ic - 1) * strides[1] + npts
+                           if npts and oc and ic else 0)
         if ncomp != ncomp_expected:
             raise EvalError(f"field {name!r} holds {ncomp} component arrays, its declaration "
                             f"has {ncomp_expected}")
@@ -291,7 +294,23 @@ def _bind(vs: Sequence[Any], env: Env, components=None):
     stores = []
     for info in plan.fields:
         stores.append(_Storage(fields[info.name], info.n_components, info.name))
+    _check_disjoint(stores, [info.name for info in plan.fields])
     return plan, kern, stores
+
+
+def _check_disjoint(stores: list, names: list[str]) -> None:
+    """Distinct fields must not share memory (exact aliases were merged into
+    one field above): the kernels treat every (field, component) slot as its
+    own array, as the reference's per-name numpy arrays are."""
+    spans = []
+    for s, name in zip(stores, names):
+        if s.extent:
+            spans.append((s.where, s.base, s.base + 8 * s.extent, name))
+    spans.sort()
+    for a, b in zip(spans, spans[1:]):
+        if a[0] == b[0] and b[1] < a[2]:
+            raise EvalError(f"fields {a[3]!r} and {b[3]!r} overlap in memory; distinct "
+                            "fields must be distinct arrays")
 
 
 def _launch(plan: KernelPlan, kern: Kernel, stores: list[_Storage], n: int,

@@ -367,3 +367,16 @@ def test_foreign_ir_classes_are_accepted():
     env = device_env(prog, host)
     eval_program(foreign, env)
     _check(case, env_to_host(env), want)
+
+
+def test_partially_overlapping_fields_are_rejected():
+    prog, (v,) = program("tensor A dim 3 rank 1;\ntensor B dim 3 rank 1;\nA(i) = B(i);\n")
+    from paper_1804_10120_b200.fields import TensorField
+
+    store = torch.zeros(3 * 1 * 10, dtype=torch.float64, device="cuda")
+    a = TensorField("A", prog.decls.tensors["A"], 0)
+    b = TensorField("B", prog.decls.tensors["B"], 0)
+    a.data = store[:27].view(3, 1, 9)
+    b.data = store[3:30].view(3, 1, 9)
+    with pytest.raises(EvalError, match="overlap"):
+        eval_statement(v, {"A": a, "B": b})
