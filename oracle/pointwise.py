@@ -16,7 +16,7 @@ import math
 
 import numpy as np
 
-from .numpy_eval import _k, _leaf_slots, _val, lhs_bindings, odometer, prepare  # noqa: F401
+from .numpy_eval import _k, _leaf_slots, lhs_bindings, prepare
 
 
 def _point(e, v, env, binding, x, touched):

@@ -579,11 +579,3 @@ def _statement_comment(v) -> str:
         return signature(v).replace("\n", " ")
     except Exception:  # reference-built trees: the comment is informational
         return repr(v.stmt)[:200]
-
-
-def flops_of(statements: Sequence[Any]) -> int:
-    return lower_program(statements).flops_per_point
-
-
-def env_fingerprint() -> str:
-    return os.environ.get("TLK_DEFINES", "")

@@ -2,7 +2,6 @@
 declares, compiles with NVRTC host-only, and fails loudly (no fallback)
 where a GPU is required."""
 
-import ctypes
 import re
 from pathlib import Path
 

@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1804_10120_b200.partition import all_slabs, domain_bounds, slab_bounds
+from paper_1804_10120_b200.partition import all_slabs, domain_bounds
 
 
 @pytest.mark.parametrize("n", [0, 1, 255, 256, 257, 1000, 1 << 20, (1 << 28) + 3])

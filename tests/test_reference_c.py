@@ -4,7 +4,7 @@ for bench.py — and the slab-threaded driver does not change a bit."""
 
 import pytest
 
-from helpers import golden_io, manifest, program, same_bits
+from helpers import golden_io, manifest, same_bits
 from oracle import refc
 
 PROGRAM_CASES = {"c1_dtg": "c1_dtg", "c2_maxwell": "c2_maxwell",
