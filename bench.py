@@ -58,6 +58,8 @@ def parse_args():
                     help="target CPU work of the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config (C1-C4, C2 N sweep) device timings")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
                     help="process-group backend (gloo + --same-device: multi-rank path "
@@ -265,15 +267,20 @@ def run_ours(args, dist: Dist) -> dict | None:
         except Exception:
             traffic = None
 
+    del env
+    torch.cuda.empty_cache()
     e2e = None
     if not args.no_e2e:
-        del env
-        torch.cuda.empty_cache()
         e2e = run_e2e(args, dist, vs, n_local)
 
-    cpu = None
+    cpu = port = None
     if not args.no_cpu and dist.world == 1:
         cpu = cpu_baseline(args)
+        port = cpu_port_baseline(args)
+
+    configs = None
+    if not args.no_configs and dist.world == 1:
+        configs = run_configs()
 
     if dist.rank != 0:
         return None
@@ -321,6 +328,8 @@ def run_ours(args, dist: Dist) -> dict | None:
         },
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "cpu_baseline_numpy_port": port,
+        "configs": configs,
         "clocks": clk,
         "gpu_launches": launches,
     }
@@ -424,6 +433,94 @@ def cpu_baseline(args) -> dict:
     return {"value": args.cpu_sample / t, "unit": "gridpoints/s", "cores": cores, "kind": kind,
             "sample": f"P2 on {args.cpu_sample} points x {len(times)} runs "
                       f"(median {t * 1e3:.1f} ms/run): {what}"}
+
+
+def cpu_port_baseline(args) -> dict:
+    """The reference evaluator's algorithm (numpy, one op per node per
+    component, evaluator.py:122-236) as restated by the oracle, 1 thread —
+    the paper's "NonAccel" analogue, beside the emitted-C "AccelCPU" one."""
+    from oracle import numpy_eval
+
+    n = max(1, args.cpu_sample // 4)
+    vs, env = _cpu_sample_env(n)
+    numpy_eval.eval_program(vs, env)
+    times = []
+    t_all = time.perf_counter()
+    while time.perf_counter() - t_all < 3.0 and len(times) < 20:
+        t0 = time.perf_counter()
+        numpy_eval.eval_program(vs, env)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": n / t, "unit": "gridpoints/s", "cores": 1, "kind": "port",
+            "sample": f"P2 on {n} points x {len(times)} runs (median {t * 1e3:.1f} ms): "
+                      "oracle/numpy_eval.py restatement of the reference evaluator"}
+
+
+def run_configs() -> dict:
+    """Device time of every BASELINE config on this GPU (CUDA-graph replay,
+    L2 flushed before each replay, median of 11 after 1 discarded)."""
+    import torch
+
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200 import capture_graph, eval_batch, eval_program
+    from paper_1804_10120_b200.evaluator import plan_for
+
+    peak, _ = measured_peak()
+    flush = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+
+    def timed(fn):
+        g = capture_graph(fn)
+        ts = []
+        for _ in range(12):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+        return statistics.median(ts[1:])
+
+    def fields(text, n, seed=SEED):
+        prog, vs = tb.load(text)
+        targets = {v.stmt.lhs.field for v in vs}
+        env = tb.make_env(prog, "__none__", 0, seed)
+        for f in env.values():
+            f.resize(n)
+            if f.name not in targets:
+                f.data.uniform_()
+        return vs, env
+
+    out = {}
+
+    def record(key, n, t, plan):
+        gbs = plan.bytes_per_point * n / t / 1e9
+        out[key] = {"N": n, "us": round(t * 1e6, 2), "gridpoints_per_s": n / t,
+                    "hbm_gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                    "variant": plan.variant.tag() if plan.variant else None}
+
+    for key, text, n in (("C1_dtg_64^3", tb.DTG, 64**3),
+                         ("C3_christoffel_128^3", tb.CHRISTOFFEL, 128**3),
+                         ("C2_maxwell_1e3", tb.MAXWELL, 10**3),
+                         ("C2_maxwell_1e4", tb.MAXWELL, 10**4),
+                         ("C2_maxwell_1e5", tb.MAXWELL, 10**5),
+                         ("C2_maxwell_1e6", tb.MAXWELL, 10**6),
+                         ("C2_maxwell_1e7", tb.MAXWELL, 10**7),
+                         ("C2_maxwell_1e8", tb.MAXWELL, 10**8)):
+        vs, env = fields(text, n)
+        record(key, n, timed(lambda: eval_program(vs, env)), plan_for(vs, env))
+        del env
+        torch.cuda.empty_cache()
+    prog, vs = tb.load(tb.P2)
+    envs = []
+    for d in range(512):
+        _, env = fields(tb.P2, 16**3, SEED + d)
+        envs.append(env)
+    record("C4_p2_512x16^3_one_launch", 512 * 16**3, timed(lambda: eval_batch(vs, envs)),
+           plan_for(vs, envs[0]))
+    out["method"] = ("CUDA-graph replay, L2 flushed (256 MB write) before each replay, "
+                     "median of 11; frac of MEASURED_PEAKS hbm_gbs")
+    return out
 
 
 def run_reference(args, dist: Dist) -> dict | None:

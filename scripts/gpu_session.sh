@@ -12,7 +12,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-    python bench.py --points 33554432 --steps 3 --warmup 1 --no-e2e --no-cpu > $OUT/ncu_launch_bench.json 2>&1
+    python bench.py --points 33554432 --steps 3 --warmup 1 --no-e2e --no-cpu --no-configs > $OUT/ncu_launch_bench.json 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tlk_flat -s 1 -c 1 \
-    -o $OUT/prof_p2 python bench.py --points 33554432 --steps 2 --warmup 1 --no-e2e --no-cpu > $OUT/ncu_full.log 2>&1
+    -o $OUT/prof_p2 python bench.py --points 33554432 --steps 2 --warmup 1 --no-e2e --no-cpu --no-configs > $OUT/ncu_full.log 2>&1
 echo done > $OUT/DONE
