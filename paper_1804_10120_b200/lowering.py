@@ -54,7 +54,7 @@ from .symmetry import SymmetrySpec, iter_canonical, slot_index
 
 TEMPLATE_PATH = Path(__file__).with_name("csrc") / "tlk_template.cuh"
 LOWERING_VERSION = "tlk-1"
-MAX_PARAM_SLOTS = 500  # 8 + 8*500 bytes < 4 KiB kernel parameter block
+MAX_PARAM_SLOTS = 4000  # 8 + 8*4000 bytes <= 32764-byte parameter block (CUDA >= 12.1, sm_70+)
 
 SLOT_READ = 1
 SLOT_WRITE = 2

@@ -380,3 +380,21 @@ def test_partially_overlapping_fields_are_rejected():
     b.data = store[3:30].view(3, 1, 9)
     with pytest.raises(EvalError, match="overlap"):
         eval_statement(v, {"A": a, "B": b})
+
+
+def test_parameter_block_beyond_4kib():
+    # 513 component pointers -> a 4112-byte parameter block (CUDA >= 12.1
+    # allows up to 32764 bytes on sm_70+)
+    src = ("tensor A dim 4 rank 4;\ntensor B dim 4 rank 4;\nfield w;\n"
+           "A(a, b, c, d) = B(d, c, b, a)*w + B(a, b, c, d);\n")
+    prog, vs = program(src)
+    host = random_host_env(prog, 1001, 3)
+    want = {k: a.copy() for k, a in host.items()}
+    numpy_eval.eval_program(vs, want)
+    env = device_env(prog, host)
+    eval_program(vs, env)
+    assert same_bits(env_to_host(env)["A"], want["A"])
+    envs = [device_env(prog, host) for _ in range(3)]  # and the batch table path
+    eval_batch(vs, envs)
+    for e in envs:
+        assert same_bits(env_to_host(e)["A"], want["A"])
