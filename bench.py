@@ -111,6 +111,14 @@ class Dist:
             self.pg.destroy_process_group()
 
 
+class _RefDist:
+    """Rank/world view for the CPU reference arm (no process group)."""
+
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+
+
 def slab(n_total: int, rank: int, world: int, align: int = 256) -> tuple[int, int]:
     from paper_1804_10120_b200.partition import slab_bounds
 
@@ -656,9 +664,18 @@ def main() -> int:
     if args.sweep:
         run_sweep(args)
         return 0
+    if args.impl == "reference":
+        # CPU-only arm: rank 0 alone works (no process group needed); the
+        # other torchrun ranks exit 0 without work
+        if int(os.environ.get("RANK", "0")) != 0:
+            return 0
+        line = run_reference(args, _RefDist())
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return 0
     dist = Dist(args.dist_backend, args.same_device)
     try:
-        line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
+        line = run_ours(args, dist)
         if line is not None:
             print(json.dumps(line), flush=True)
     finally:
