@@ -541,6 +541,13 @@ def run_configs() -> dict:
         envs.append(env)
     record("C4_p2_512x16^3_one_launch", 512 * 16**3, timed(lambda: eval_batch(vs, envs)),
            plan_for(vs, envs[0]))
+    del envs
+    # the chained variant (P3: Gamma -> nabla beta -> dt g)
+    prog3, vs3 = tb.load(tb.P3)
+    envs3 = [fields(tb.P3, 16**3, SEED + d)[1] for d in range(512)]
+    record("C4_p3_chain_512x16^3_one_launch", 512 * 16**3,
+           timed(lambda: eval_batch(vs3, envs3)), plan_for(vs3, envs3[0]))
+    del envs3
     out["method"] = ("CUDA-graph replay, L2 flushed (256 MB write) before each replay, "
                      "median of 11; hbm_gbs/frac use the fused program's algorithmic bytes "
                      "(for *_arrays_mode that is the paper's BW_eff, not the traffic)")
