@@ -121,6 +121,9 @@ void tlb_batch_destroy(tlb_batch* b);
 int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_ptrs,
                   long long slab, void* stream);
 
+/* Free the host-staging buffers (tlb_exec_host) of the current context. */
+int tlb_release_staging(void);
+
 /* ---- reference-harness bindings --------------------------------------------
  *
  * Lets the reference's UNCHANGED conformance harness (pkg/harness/tl_harness.c)

@@ -644,6 +644,20 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
   return 0;
 }
 
+int tlb_release_staging(void) {
+  if (!g_driver_ok) return 0;
+  CUcontext ctx = nullptr;
+  g_cu.CtxGetCurrent(&ctx);
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  auto it = g_ctx.find(ctx);
+  if (it != g_ctx.end() && it->second.scratch) {
+    CU(g_cu.MemFree(it->second.scratch), "cuMemFree(staging)");
+    it->second.scratch = 0;
+    it->second.scratch_bytes = 0;
+  }
+  return 0;
+}
+
 int tlb_harness_call(tlb_harness_kernel* hk, long n, double** const* tensors,
                      const double* const* scalars) {
   if (!hk) return fail("tlb_harness_call: null kernel");

@@ -36,7 +36,10 @@ from .symmetry import SymmetrySpec, alias_table, component_count
 
 MANIFEST_NAME = "tloops_manifest.tsv"
 BINDINGS_NAME = "tloops_bindings_b200.c"
-BACKENDS = ("b200",)
+# "cuda" is accepted as the reference's name for the GPU backend; the
+# reference's CPU C emission ("c") is not part of this package (the
+# reference's own emitted C is the CPU baseline, oracle/build_ref.py)
+BACKENDS = ("b200", "cuda")
 INCLUDE_DIR = Path(__file__).resolve().parent.parent / "include"
 
 
@@ -147,7 +150,9 @@ class Registry:
 
     def write_all(self, out_dir, backend: str = "b200") -> list[Path]:
         if backend not in BACKENDS:
-            raise ValueError(f"backend must be one of {BACKENDS}, got {backend!r}")
+            raise ValueError(f"backend must be one of {BACKENDS}, got {backend!r} (the CPU "
+                             "C backend of the reference is not provided: this package runs "
+                             "statements on the GPU)")
         if not self.entries:
             raise ValueError("registry is empty: nothing to generate")
         out = Path(out_dir)

@@ -35,7 +35,7 @@ EXPORTED = (
     "tlb_compile", "tlb_kernel_log", "tlb_kernel_cubin", "tlb_kernel_destroy",
     "tlb_kernel_set_slots", "tlb_kernel_attrs", "tlb_launch", "tlb_batch_create",
     "tlb_batch_launch", "tlb_batch_destroy", "tlb_exec_host", "tlb_fill_uniform",
-    "tlb_harness_call",
+    "tlb_harness_call", "tlb_release_staging",
 )
 
 
@@ -89,6 +89,7 @@ def lib() -> ctypes.CDLL:
                                           c_ll, c_vp]),
                 "tlb_fill_uniform": (c_int, [c_vp, c_ll, ctypes.c_ulonglong, ctypes.c_ulonglong,
                                              c_ll, c_vp]),
+                "tlb_release_staging": (c_int, []),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -267,6 +268,11 @@ def get_kernel(plan: KernelPlan) -> Kernel:
 
 def all_kernels() -> list[Kernel]:
     return list(_kernels.values())
+
+
+def release_staging() -> None:
+    """Free the device staging buffers used for host-resident fields."""
+    check(lib().tlb_release_staging(), "tlb_release_staging")
 
 
 def fill_uniform(t, seed: int, stream_id: int, offset: int = 0, stream: int | None = None):
