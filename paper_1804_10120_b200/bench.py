@@ -14,6 +14,8 @@ every run (CUDA events when no clock is injected).
 
 from __future__ import annotations
 
+import csv
+import json
 import time
 from dataclasses import dataclass
 from statistics import median
@@ -304,3 +306,16 @@ def sweep(entries: Sequence[SuiteEntry], gridsizes: Sequence[int] = DEFAULT_GRID
           seed: int = DEFAULT_SEED) -> list[BenchResult]:
     return [run(e, n, reps=reps, mode=m, seed=seed)
             for e in entries for m in modes for n in gridsizes]
+
+
+def write_csv(results: Iterable[BenchResult], out) -> None:
+    """CSV with the reference's columns (bench.py:307-312)."""
+    w = csv.writer(out)
+    w.writerow(CSV_COLUMNS)
+    for r in results:
+        w.writerow([r.name, r.mode, r.gridsize, repr(r.t), repr(r.bw_eff), r.n_e, r.n_d])
+
+
+def write_json(results: Iterable[BenchResult], out) -> None:
+    json.dump([dict(zip(CSV_COLUMNS, r.row())) for r in results], out, indent=2)
+    out.write("\n")

@@ -1,0 +1,74 @@
+"""CLI mirror: same diagnostics/exit codes as the reference CLI (checked
+against the reference package where importable), and `eval` writes the
+container the reference writes (GPU)."""
+
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+from helpers import GOLDEN, manifest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _cli(*args, module="paper_1804_10120_b200", env=None):
+    return subprocess.run([sys.executable, "-m", module, *args], capture_output=True, text=True,
+                          cwd=ROOT, timeout=600, env=env)
+
+
+@pytest.mark.parametrize("k", range(len(manifest()["bad_programs"])))
+def test_check_diagnostics_and_exit_code(k, tmp_path, capsys):
+    from paper_1804_10120_b200.cli import main
+
+    src = manifest()["bad_programs"][k]["source"]
+    f = tmp_path / "p.tl"
+    f.write_text(src)
+    assert main(["check", str(f)]) == 1
+    want = [f"{f}:{ln}:{col}: {msg}" for ln, col, msg in manifest()["bad_programs"][k]["diagnostics"]]
+    assert capsys.readouterr().err.splitlines() == want
+
+
+def test_check_validation_codes_and_io_errors(tmp_path):
+    f = tmp_path / "p.tl"
+    f.write_text("tensor A dim 3 rank 2;\nA(i, i) = 0;\n")
+    res = _cli("check", str(f))
+    assert res.returncode == 1 and "[repeated-lhs-index]" in res.stderr
+    assert _cli("check", str(tmp_path / "missing.tl")).returncode == 2
+    f.write_text(manifest()["cases"]["c4_p2"]["source"])
+    assert _cli("check", str(f)).returncode == 0
+
+
+def test_check_matches_reference_cli(tmp_path):
+    pytest.importorskip("tlang.cli")
+    import os
+
+    env = dict(os.environ, PYTHONPATH="/root/reference/pkg/src")
+    for src in (manifest()["cases"]["c4_p3"]["source"], "tensor A dim 3 rank 1;\nA(i) = B(i);\n",
+                "tensor A dim 3 rank 1;\ntensor B dim 3 rank 2;\nA(i) = B(i);\n"):
+        f = tmp_path / "p.tl"
+        f.write_text(src)
+        mine, ref = _cli("check", str(f)), _cli("check", str(f), module="tlang.cli", env=env)
+        assert (mine.returncode, mine.stderr) == (ref.returncode, ref.stderr)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["c4_p3", "c2_maxwell", "seq_augmented"])
+@pytest.mark.parametrize("per_component", [False, True])
+def test_eval_writes_the_reference_container(case, per_component, tmp_path):
+    from paper_1804_10120_b200 import tldf
+
+    spec = manifest()["cases"][case]
+    f = tmp_path / "p.tl"
+    f.write_text(spec["source"])
+    out = tmp_path / "out.tldf"
+    args = ["eval", str(f), "--data", str(GOLDEN / f"{case}.in.tldf"), "--out", str(out)]
+    res = _cli(*args, *(["--per-component"] if per_component else []))
+    assert res.returncode == 0, res.stderr
+    # expected bytes: the input container with every target replaced by the
+    # reference's output, in the same order (reference cli.py:77-104)
+    env = tldf.read(GOLDEN / f"{case}.in.tldf", device="cpu")
+    for name, fld in tldf.read(GOLDEN / f"{case}.out.tldf", device="cpu").items():
+        env[name] = fld
+    assert out.read_bytes() == tldf.dumps(env)
