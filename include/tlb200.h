@@ -110,7 +110,9 @@ int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
 int tlb_batch_create(tlb_kernel* k, int ndom, const void* const* field_bases,
                      const long long* pitches, const long long* ns, void* stream,
                      tlb_batch** out);
-int tlb_batch_launch(tlb_batch* b, int threads, void* stream);
+/* vec: 0 = 2-point variant when every slot of every domain is 16-byte
+ * aligned, 1 = force the 1-point variant. */
+int tlb_batch_launch(tlb_batch* b, int vec, int threads, void* stream);
 void tlb_batch_destroy(tlb_batch* b);
 
 /* Host-resident fields: comp_ptrs[f][c] is the host address of canonical

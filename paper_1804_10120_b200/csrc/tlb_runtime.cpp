@@ -533,7 +533,7 @@ int tlb_batch_create(tlb_kernel* k, int ndom, const void* const* field_bases,
   return 0;
 }
 
-int tlb_batch_launch(tlb_batch* b, int threads, void* stream) {
+int tlb_batch_launch(tlb_batch* b, int vec, int threads, void* stream) {
   if (!b) return fail("tlb_batch_launch: null batch");
   if (ensure(true)) return 1;
   CUcontext ctx;
@@ -543,9 +543,10 @@ int tlb_batch_launch(tlb_batch* b, int threads, void* stream) {
   if (ctx_state(ctx, &st)) return 1;
   Loaded* L;
   if (load_module(b->k, ctx, &L)) return 1;
-  const int e = b->vec2 ? BATCH_V2 : BATCH_V1;
+  const bool v2 = b->vec2 && vec != 1;
+  const int e = v2 ? BATCH_V2 : BATCH_V1;
   if (threads <= 0) threads = kDefaultThreads;
-  long long units = b->vec2 ? (b->max_n + 1) / 2 : b->max_n;
+  long long units = v2 ? (b->max_n + 1) / 2 : b->max_n;
   long long gx = std::max(1LL, (units + threads - 1) / threads);
   long long gy = std::min<long long>(b->ndom, 65535);
   // optional cap of the grid at a few waves (TLB_BATCH_WAVES; default 0 =

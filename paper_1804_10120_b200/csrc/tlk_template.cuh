@@ -148,10 +148,45 @@ tlk_flat_v2(const tlk_flat_params prm) {
 }
 
 // table: per domain { long long n; double* p[TLK_NSLOTS]; } (tlb_batch_create)
+// TLK_BATCH_PTRS 0: the block stages the domain's slot pointers in shared
+//                   memory (one barrier pair per domain)            [default]
+//                1: every thread reads them straight from the (read-only,
+//                   L1-resident) table: no barriers, so pointer fetches of
+//                   one warp overlap data traffic of the others
+#ifndef TLK_BATCH_PTRS
+#define TLK_BATCH_PTRS 0
+#endif
+
+struct tlk_table_ptrs {
+  const long long* __restrict__ rec;
+  struct view {
+    const long long* __restrict__ r;
+    __device__ __forceinline__ double* operator[](int j) const {
+      return reinterpret_cast<double*>(__ldg(r + 1 + j));
+    }
+  } p;
+};
+
+template <typename T, typename P>
+__device__ __forceinline__ void tlk_domain(const P& ptrs, const long long n, const long long stride) {
+  if constexpr (sizeof(T) == 16) {
+    const long long pairs = n >> 1;
+    TLK_LOOP
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride)
+      tlk_point<T>(ptrs, i << 1);
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) tlk_point<double>(ptrs, n - 1);
+  } else {
+    TLK_LOOP
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += stride)
+      tlk_point<double>(ptrs, x);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void tlk_batch_body(const long long* __restrict__ table, int ndom) {
-  __shared__ double* sp[TLK_NSLOTS];
   const long long stride = (long long)gridDim.x * blockDim.x;
+#if TLK_BATCH_PTRS == 0
+  __shared__ double* sp[TLK_NSLOTS];
   for (int d = blockIdx.y; d < ndom; d += gridDim.y) {
     const long long* rec = table + (long long)d * (TLK_NSLOTS + 1);
     __syncthreads();  // readers of the previous domain's pointers are done
@@ -159,19 +194,15 @@ __device__ __forceinline__ void tlk_batch_body(const long long* __restrict__ tab
       sp[j] = reinterpret_cast<double*>(rec[1 + j]);
     const long long n = rec[0];
     __syncthreads();
-    const tlk_shared_ptrs P{sp};
-    if constexpr (sizeof(T) == 16) {
-      const long long pairs = n >> 1;
-      TLK_LOOP
-      for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride)
-        tlk_point<T>(P, i << 1);
-      if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) tlk_point<double>(P, n - 1);
-    } else {
-      TLK_LOOP
-      for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += stride)
-        tlk_point<double>(P, x);
-    }
+    tlk_domain<T>(tlk_shared_ptrs{sp}, n, stride);
   }
+#else
+  for (int d = blockIdx.y; d < ndom; d += gridDim.y) {
+    const long long* rec = table + (long long)d * (TLK_NSLOTS + 1);
+    const tlk_table_ptrs P{rec, {rec}};
+    tlk_domain<T>(P, __ldg(rec), stride);
+  }
+#endif
 }
 
 extern "C" __global__ void __launch_bounds__(TLK_THREADS)

@@ -453,10 +453,12 @@ class Variant:
     ldmode: int = 0
     vec: int = 2
     waves: int = 1
+    batch_vec: int = 2  # points per thread of the multi-domain batch entry
+    batch_ptrs: int = 0  # TLK_BATCH_PTRS: 0 shared-memory staging, 1 direct table reads
 
     def tag(self) -> str:
         return (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
-                f"v{self.vec}w{self.waves}")
+                f"v{self.vec}w{self.waves}b{self.batch_vec}{self.batch_ptrs}")
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -500,6 +502,10 @@ def _env_variant(v: Variant) -> Variant:
         kw["vec"] = int(env["TLK_VEC"])
     if "TLK_WAVES" in env:
         kw["waves"] = int(env["TLK_WAVES"])
+    if "TLK_BATCH_VEC" in env:
+        kw["batch_vec"] = int(env["TLK_BATCH_VEC"])
+    if "TLK_BATCH_PTRS" in env:
+        kw["batch_ptrs"] = int(env["TLK_BATCH_PTRS"])
     return Variant(**{**v.__dict__, **kw}) if kw else v
 
 
@@ -549,6 +555,7 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         header.append("// " + _statement_comment(v))
     header.append(f"#define TLK_NSLOTS {n_slots}")
     header.append(f"#define TLK_LDMODE {variant.ldmode}")
+    header.append(f"#define TLK_BATCH_PTRS {variant.batch_ptrs}")
     src = "\n".join(header) + "\n" + template_text().replace("// @@TLK_BODY@@", body)
     plan = KernelPlan(src, low.fields, slot_field, slot_comp, list(b.slot_flags), b.flops, n_ops,
                       len(statements), lhs_fields=lhs_fields, variant=variant, phases=phases)

@@ -83,7 +83,7 @@ def lib() -> ctypes.CDLL:
                 "tlb_batch_create": (c_int, [c_vp, c_int, ctypes.POINTER(c_vp),
                                              ctypes.POINTER(c_ll), ctypes.POINTER(c_ll), c_vp,
                                              ctypes.POINTER(c_vp)]),
-                "tlb_batch_launch": (c_int, [c_vp, c_int, c_vp]),
+                "tlb_batch_launch": (c_int, [c_vp, c_int, c_int, c_vp]),
                 "tlb_batch_destroy": (None, [c_vp]),
                 "tlb_exec_host": (c_int, [c_vp, c_ll, ctypes.POINTER(ctypes.POINTER(c_vp)),
                                           c_ll, c_vp]),
@@ -172,6 +172,7 @@ class Kernel:
         self.vec = 1 if (var is not None and var.vec == 1) else 0
         if var is not None and var.waves > 1 and self.max_blocks == 0:
             self.max_blocks = -var.waves
+        self.batch_vec = 1 if (var is not None and var.batch_vec == 1) else 0
 
     @property
     def log(self) -> str:
@@ -237,7 +238,8 @@ class Batch:
 
     def launch(self, stream: int, threads: int | None = None) -> None:
         threads = self.kernel.threads if threads is None else threads
-        check(lib().tlb_batch_launch(self.handle, threads, stream), "tlb_batch_launch")
+        check(lib().tlb_batch_launch(self.handle, self.kernel.batch_vec, threads, stream),
+              "tlb_batch_launch")
         self.kernel.launches += 1
 
     def __del__(self):
