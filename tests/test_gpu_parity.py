@@ -398,3 +398,33 @@ def test_parameter_block_beyond_4kib():
     eval_batch(vs, envs)
     for e in envs:
         assert same_bits(env_to_host(e)["A"], want["A"])
+
+
+@pytest.mark.parametrize("bvec", [1, 2])
+@pytest.mark.parametrize("bptrs", [0, 1])
+@pytest.mark.parametrize("name", ["c4_p2", "c4_p3", "c1_dtg_odd", "seq_augmented"])
+def test_batch_entry_variants_bit_exact(name, bptrs, bvec):
+    from paper_1804_10120_b200.evaluator import _bind, _prepare
+    from paper_1804_10120_b200.lowering import Variant, lower_program
+    from paper_1804_10120_b200.runtime import Batch, Kernel
+
+    case = manifest()["cases"][name]
+    prog, vs = program(case["source"])
+    host, want = golden_io(name)
+    envs = [device_env(prog, host) for _ in range(3)]
+    kern = None
+    bases, pitches, ns = [], [], []
+    for env in envs:
+        sizes = {_prepare(v, env)[1] for v in vs}
+        if len(sizes) != 1:
+            pytest.skip("not fusable")
+        _, _, stores = _bind(vs, env)
+        bases.append([s.base for s in stores])
+        pitches.append([s.pitch for s in stores])
+        ns.append(sizes.pop())
+    plan = lower_program(vs, variant=Variant(batch_ptrs=bptrs, batch_vec=bvec))
+    kern = Kernel(plan)
+    stream = torch.cuda.current_stream().cuda_stream
+    Batch(kern, bases, pitches, ns, stream).launch(stream)
+    for env in envs:
+        _check(case, env_to_host(env), want)
