@@ -453,7 +453,7 @@ class Variant:
     ldmode: int = 0
     vec: int = 2
     waves: int = 1
-    batch_vec: int = 2  # points per thread of the multi-domain batch entry
+    batch_vec: int = 1  # points per thread of the multi-domain batch entry
     batch_ptrs: int = 0  # TLK_BATCH_PTRS: 0 shared-memory staging, 1 direct table reads
 
     def tag(self) -> str:
@@ -478,7 +478,11 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
       every load is hoisted to the top, otherwise each statement's loads
       wait for the previous statement's stores (2.1x on P3);
     * with read-modify-write slots the restrict-free 2-point body over 4
-      waves is used.
+      waves is used;
+    * the multi-domain batch entry always runs one point per thread with the
+      domain's slot pointers staged in shared memory (small 16^3 domains:
+      twice the blocks in flight hide the per-domain pointer fetch; C4 P2
+      5.64 -> 6.10 TB/s, P3 chain 5.10 -> 5.87 TB/s, profiles/r01/tune_batch.jsonl).
     """
     arrays = reads + writes
     if n_ops <= 1.5 * arrays:
