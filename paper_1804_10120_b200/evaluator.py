@@ -419,8 +419,32 @@ def _fast_record(key, vs, kern: Kernel, stores: list, n: int) -> None:
 
 
 # -------------------------------------------------------------- public API --
+# TLB_NVTX=1 wraps every public evaluation in an NVTX range (for nsys/ncu
+# timelines); otherwise the functions are left untouched (no overhead).
 
 
+def _nvtx(fn):
+    import os
+
+    if os.environ.get("TLB_NVTX", "0") != "1":
+        return fn
+    import functools
+
+    import torch
+
+    @functools.wraps(fn)
+    def wrapped(*a, **kw):
+        torch.cuda.nvtx.range_push(f"tlb.{fn.__name__}")
+        try:
+            return fn(*a, **kw)
+        finally:
+            torch.cuda.nvtx.range_pop()
+
+    return wrapped
+
+
+
+@_nvtx
 def eval_statement(v, env: Env, *, chunk: int | None = None, threads: int | None = None) -> None:
     """Execute one statement in place over `env` as one fused GPU launch.
 
@@ -443,6 +467,7 @@ def eval_statement(v, env: Env, *, chunk: int | None = None, threads: int | None
         _fast_record(_fast_key((v,), env), (v,), kern, stores, n)
 
 
+@_nvtx
 def eval_statement_per_component(v, env: Env) -> None:
     """The paper's "Arrays" pathway (reference evaluator.py:239-257): one
     GPU launch per canonical LHS component, each a full grid traversal,
@@ -454,6 +479,7 @@ def eval_statement_per_component(v, env: Env) -> None:
         _launch(plan, kern, stores, n)
 
 
+@_nvtx
 def eval_program(vs: Sequence[Any], env: Env) -> None:
     """Execute statements in order, fused into ONE kernel when they share a
     gridsize (else one launch per statement).  Bitwise identical to
@@ -503,6 +529,7 @@ class _BatchCache:
 _batches = _BatchCache()
 
 
+@_nvtx
 def eval_batch(vs, envs: Sequence[Env]) -> None:
     """Execute a statement (or a program) over many independent subdomains
     in ONE launch.  ``envs[d]`` is subdomain d's data environment; the result
