@@ -464,6 +464,41 @@ def cpu_port_baseline(args) -> dict:
                       "oracle/numpy_eval.py restatement of the reference evaluator"}
 
 
+class L2Flush:
+    """Leave the 126 MB L2 cold and clean: write 256 MB (evicts everything),
+    then read another 256 MB (the flush's own dirty lines are written back
+    here, not inside the next timed kernel)."""
+
+    def __init__(self):
+        import torch
+
+        self.w = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+        self.r = torch.ones(1 << 25, dtype=torch.float64, device="cuda")
+
+    def __call__(self):
+        self.w.zero_()
+        self.r.sum()
+
+
+def back_to_back(fn, k: int = 20) -> float:
+    """Seconds per call of `fn` over k calls captured in one graph (steady
+    state: each launch pays for the previous one's write-backs)."""
+    import torch
+
+    from paper_1804_10120_b200 import capture_graph
+
+    g = capture_graph(lambda: [fn() for _ in range(k)])
+    ts = []
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3 / k)
+    return statistics.median(ts[1:])
+
+
 def run_configs() -> dict:
     """Device time of every BASELINE config on this GPU (CUDA-graph replay,
     L2 flushed before each replay, median of 11 after 1 discarded)."""
@@ -474,20 +509,20 @@ def run_configs() -> dict:
     from paper_1804_10120_b200.evaluator import plan_for
 
     peak, _ = measured_peak()
-    flush = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+    flush = L2Flush()
 
     def timed(fn):
         g = capture_graph(fn)
         ts = []
         for _ in range(12):
-            flush.zero_()
+            flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             g.replay()
             b.record()
             b.synchronize()
             ts.append(a.elapsed_time(b) / 1e3)
-        return statistics.median(ts[1:])
+        return statistics.median(ts[1:]), back_to_back(fn)
 
     def fields(text, n, seed=SEED):
         prog, vs = tb.load(text)
@@ -502,9 +537,12 @@ def run_configs() -> dict:
     out = {}
 
     def record(key, n, t, plan):
+        t, t_b2b = t
         gbs = plan.bytes_per_point * n / t / 1e9
         out[key] = {"N": n, "us": round(t * 1e6, 2), "gridpoints_per_s": n / t,
                     "hbm_gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                    "us_b2b": round(t_b2b * 1e6, 2),
+                    "frac_b2b": round(plan.bytes_per_point * n / t_b2b / 1e9 / peak, 4),
                     "variant": plan.variant.tag() if plan.variant else None}
 
     for key, text, n in (("C1_dtg_64^3", tb.DTG, 64**3),
@@ -548,9 +586,16 @@ def run_configs() -> dict:
     record("C4_p3_chain_512x16^3_one_launch", 512 * 16**3,
            timed(lambda: eval_batch(vs3, envs3)), plan_for(vs3, envs3[0]))
     del envs3
-    out["method"] = ("CUDA-graph replay, L2 flushed (256 MB write) before each replay, "
-                     "median of 11; hbm_gbs/frac use the fused program's algorithmic bytes "
-                     "(for *_arrays_mode that is the paper's BW_eff, not the traffic)")
+    tiny = torch.zeros(1, device="cuda")
+    out["floor_us"] = round(timed(lambda: tiny.add_(1.0))[0] * 1e6, 2)
+    out["method"] = ("us/frac: one CUDA-graph replay bracketed by events after an L2 flush "
+                     "(256 MB write, then 256 MB read: L2 cold and clean, so no write-back of "
+                     "the flush's dirty lines is billed to the kernel), median of 11; "
+                     "floor_us: the same measurement of a graph holding one 1-element kernel "
+                     "(graph launch + event overhead); us_b2b/frac_b2b: steady state, 20 "
+                     "back-to-back launches in one graph (inputs re-read from L2 when the "
+                     "working set fits); hbm_gbs/frac use the fused program's algorithmic "
+                     "bytes (for *_arrays_mode that is the paper's BW_eff, not the traffic)")
     return out
 
 
@@ -606,14 +651,14 @@ def run_sweep(args) -> None:
     from paper_1804_10120_b200.evaluator import plan_for
 
     peak, _ = measured_peak()
-    flush = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")  # 256 MB > L2
+    flush = L2Flush()
 
     def timed(fn, reps=21, flush_l2=True):
         g = capture_graph(fn)
         ts = []
         for _ in range(reps):
             if flush_l2:
-                flush.zero_()
+                flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             g.replay()

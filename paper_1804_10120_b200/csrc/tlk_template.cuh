@@ -78,6 +78,8 @@ template <> __device__ __forceinline__ double2 tl_splat<double2>(double c) { ret
 #endif
 
 template <typename T> __device__ __forceinline__ T tl_ld(const double* p);
+// TLK_LDMODE 3 (staged entry): plain dereference, so reads of the shared-
+// memory tiles compile to LDS and the global tail path to LDG
 template <> __device__ __forceinline__ double tl_ld<double>(const double* p) {
 #if TLK_LDMODE == 0
   return __ldcs(p);
@@ -214,3 +216,83 @@ extern "C" __global__ void __launch_bounds__(TLK_THREADS)
 tlk_batch_v2(const long long* __restrict__ table, int ndom) {
   tlk_batch_body<double2>(table, ndom);
 }
+
+// ------------------------------------------------ TMA-staged entry (opt-in)
+// tlk_stage_v1: persistent blocks walk tiles of TLK_THREADS points; for each
+// tile one elected thread issues one 1-D bulk copy (cp.async.bulk, the TMA
+// engine) per read slot into a TLK_NSTAGE-deep shared-memory ring, completion
+// tracked by an mbarrier (complete_tx); every thread then runs the per-point
+// body with its read slots pointing into the tile and its write slots at the
+// global arrays.  The copies of the next TLK_NSTAGE-1 tiles are in flight
+// while a tile computes.  Points past the last whole tile take the plain
+// path.  Compiled only when the lowering defines TLK_NSTAGE (with TLK_NREAD
+// and the per-slot read ordinals TLK_RORD); needs every read slot 16-byte
+// aligned (the runtime checks).
+#ifdef TLK_NSTAGE
+__device__ __forceinline__ unsigned tlk_smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+extern "C" __global__ void __launch_bounds__(TLK_THREADS)
+tlk_stage_v1(const tlk_flat_params prm) {
+  constexpr int kRord[TLK_NSLOTS] = TLK_RORD;
+  constexpr int kTile = TLK_THREADS;
+  extern __shared__ __align__(128) double tlk_sm[];  // [NSTAGE][NREAD][kTile]
+  __shared__ __align__(8) unsigned long long bar[TLK_NSTAGE];
+  const long long ntiles = prm.n / kTile;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < TLK_NSTAGE; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tlk_smem_addr(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](long long t, int s) {
+    const unsigned b = tlk_smem_addr(&bar[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(b), "r"((unsigned)(TLK_NREAD * kTile * sizeof(double))) : "memory");
+#pragma unroll
+    for (int j = 0; j < TLK_NSLOTS; ++j) {
+      if (kRord[j] < 0) continue;
+      const double* src = prm.p[j] + t * kTile;
+      double* dst = tlk_sm + ((long long)s * TLK_NREAD + kRord[j]) * kTile;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(tlk_smem_addr(dst)), "l"(src), "r"((unsigned)(kTile * sizeof(double))), "r"(b)
+          : "memory");
+    }
+  };
+  if (tid == 0)
+    for (int s = 0; s < TLK_NSTAGE; ++s) {
+      const long long t = blockIdx.x + (long long)s * gridDim.x;
+      if (t < ntiles) issue(t, s);
+    }
+  int it = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % TLK_NSTAGE;
+    const unsigned phase = (unsigned)(it / TLK_NSTAGE) & 1u;
+    const unsigned b = tlk_smem_addr(&bar[s]);
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "TLK_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra TLK_WAIT_%=;\n}" ::"r"(b), "r"(phase) : "memory");
+    tlk_flat_params q;
+    q.n = prm.n;
+#pragma unroll
+    for (int j = 0; j < TLK_NSLOTS; ++j)
+      q.p[j] = kRord[j] >= 0 ? tlk_sm + ((long long)s * TLK_NREAD + kRord[j]) * kTile
+                             : prm.p[j] + t * kTile;
+    tlk_point<double>(q, tid);
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0) {
+      const long long tn = t + (long long)TLK_NSTAGE * gridDim.x;
+      if (tn < ntiles) issue(tn, s);
+    }
+  }
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long x = ntiles * kTile + (long long)blockIdx.x * blockDim.x + tid; x < prm.n;
+       x += stride)
+    tlk_point<double>(prm, x);
+}
+#endif

@@ -157,6 +157,10 @@ class KernelPlan:
     lhs_fields: list[int] = dc_field(default_factory=list)
     variant: "Variant | None" = None
     phases: int = 1
+    # launches of at most variant.small_n points use small_variant (and, when
+    # its code generation differs, small_plan's kernel): see Variant.small_class
+    small_variant: "Variant | None" = None
+    small_plan: "KernelPlan | None" = None
 
     @property
     def n_slots(self) -> int:
@@ -455,10 +459,35 @@ class Variant:
     waves: int = 1
     batch_vec: int = 1  # points per thread of the multi-domain batch entry
     batch_ptrs: int = 0  # TLK_BATCH_PTRS: 0 shared-memory staging, 1 direct table reads
+    small_n: int = 0  # launches of <= small_n points run small_class() (0: never)
 
     def tag(self) -> str:
-        return (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
-                f"v{self.vec}w{self.waves}b{self.batch_vec}{self.batch_ptrs}")
+        t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
+             f"v{self.vec}w{self.waves}b{self.batch_vec}{self.batch_ptrs}")
+        return t + (f"s{self.small_n.bit_length() - 1}" if self.small_n else "")
+
+    def small_class(self) -> "Variant":
+        """Choices for launches of at most ``small_n`` points, where a
+        thread's dependent memory round trips, not bandwidth, set the time
+        (profiles/r01/tune_smalln.jsonl, tune_cross.jsonl):
+
+        * light kernels hoist every load to the top of the body — one
+          round trip per point instead of one per statement: Maxwell at
+          10^3-10^5 points 2.3-2.5x faster back to back, C1 at 64^3 1.1x,
+          both 1-4 % faster at 2^20;
+        * heavier kernels run one point per thread over 4 waves (a launch-
+          time choice, same cubin): twice the threads in flight — C3 at
+          128^3 +3 %, P3 +5 %, P2 +4 % at 2^20; the 2-point body wins
+          again from 2^23 points."""
+        if self.vec == 1:
+            return Variant(**{**self.__dict__, "hoist": True, "small_n": 0})
+        return Variant(**{**self.__dict__, "vec": 1, "waves": 4, "small_n": 0})
+
+    def same_code(self, other: "Variant") -> bool:
+        """Whether two variants compile to the same cubin (vec/waves are
+        launch-time choices; both entry points are in every module)."""
+        return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs)
+                == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs))
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -486,10 +515,18 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
     """
     arrays = reads + writes
     if n_ops <= 1.5 * arrays:
-        return Variant(restrict=True, hoist=False, ldmode=0, vec=1, waves=4)
+        return Variant(restrict=True, hoist=False, ldmode=0, vec=1, waves=4,
+                       small_n=SMALL_N_LIGHT)
     if rw_slots == 0:
-        return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=2, waves=4 if chained else 1)
+        return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=2, waves=4 if chained else 1,
+                       small_n=SMALL_N_HEAVY)
     return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
+
+
+# size classes (Variant.small_class): largest launch, in points, that still
+# runs the small-N choices — the crossovers in profiles/r01/tune_cross.jsonl
+SMALL_N_LIGHT = 1 << 21
+SMALL_N_HEAVY = 1 << 22
 
 
 def _env_variant(v: Variant) -> Variant:
@@ -510,6 +547,10 @@ def _env_variant(v: Variant) -> Variant:
         kw["batch_vec"] = int(env["TLK_BATCH_VEC"])
     if "TLK_BATCH_PTRS" in env:
         kw["batch_ptrs"] = int(env["TLK_BATCH_PTRS"])
+    if kw:
+        kw["small_n"] = 0  # a forced variant applies at every size ...
+    if "TLK_SMALL_N" in env:
+        kw["small_n"] = int(env["TLK_SMALL_N"])  # ... unless asked otherwise
     return Variant(**{**v.__dict__, **kw}) if kw else v
 
 
@@ -563,6 +604,13 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     src = "\n".join(header) + "\n" + template_text().replace("// @@TLK_BODY@@", body)
     plan = KernelPlan(src, low.fields, slot_field, slot_comp, list(b.slot_flags), b.flops, n_ops,
                       len(statements), lhs_fields=lhs_fields, variant=variant, phases=phases)
+    if variant.small_n:
+        sv = variant.small_class()
+        if sv.ldmode == 1 and rw:
+            sv = Variant(**{**sv.__dict__, "ldmode": 0})
+        plan.small_variant = sv
+        if not variant.same_code(sv):
+            plan.small_plan = lower_program(statements, alias, components, variant=sv)
     # identical source text can serve different slot maps (e.g. the
     # per-component kernels of one statement): the plan identity covers both
     ident = f"{src}\0{slot_field}\0{slot_comp}\0{plan.slot_flags}\0{variant.tag()}"

@@ -173,6 +173,19 @@ class Kernel:
         if var is not None and var.waves > 1 and self.max_blocks == 0:
             self.max_blocks = -var.waves
         self.batch_vec = 1 if (var is not None and var.batch_vec == 1) else 0
+        # size class (Variant.small_class): launches of <= small_n points run
+        # `small` (a second cubin when the code differs, else this one) with
+        # its own vec/waves; set by get_kernel
+        self.small_n = 0
+        self.small: "Kernel | None" = None
+        self.small_vec, self.small_max_blocks = self.vec, self.max_blocks
+
+    def _attach_small(self, small_n: int, sv, small: "Kernel | None") -> None:
+        self.small_n = small_n
+        self.small = small
+        self.small_vec = 1 if sv.vec == 1 else 0
+        self.small_max_blocks = (-sv.waves if sv.waves > 1 else 0) if self.max_blocks <= 0 \
+            else self.max_blocks
 
     @property
     def log(self) -> str:
@@ -192,17 +205,25 @@ class Kernel:
     def launch(self, n: int, bases: Sequence[int], pitches: Sequence[int], stream: int,
                vec: int | None = None, threads: int | None = None,
                max_blocks: int | None = None) -> None:
+        handle = self.handle
+        if n <= self.small_n and vec is None and max_blocks is None:
+            handle = (self.small or self).handle
+            vec, max_blocks = self.small_vec, self.small_max_blocks
         vec = self.vec if vec is None else vec
         threads = self.threads if threads is None else threads
         max_blocks = self.max_blocks if max_blocks is None else max_blocks
-        check(lib().tlb_launch(self.handle, n, _arr(c_vp, bases), _arr(c_ll, pitches), vec,
+        check(lib().tlb_launch(handle, n, _arr(c_vp, bases), _arr(c_ll, pitches), vec,
                                threads, max_blocks, stream), "tlb_launch")
         self.launches += 1
 
     def launch_arrays(self, n: int, bases, pitches, stream: int) -> None:
         """Launch with prebuilt ctypes address arrays (bound-launch fast path)."""
-        rc = _lib.tlb_launch(self.handle, n, bases, pitches, self.vec, self.threads,
-                             self.max_blocks, stream)
+        if n <= self.small_n:
+            rc = _lib.tlb_launch((self.small or self).handle, n, bases, pitches, self.small_vec,
+                                 self.threads, self.small_max_blocks, stream)
+        else:
+            rc = _lib.tlb_launch(self.handle, n, bases, pitches, self.vec, self.threads,
+                                 self.max_blocks, stream)
         if rc:
             check(rc, "tlb_launch")
         self.launches += 1
@@ -264,6 +285,9 @@ def get_kernel(plan: KernelPlan) -> Kernel:
             k = _kernels.get(key)
             if k is None:
                 k = Kernel(plan)
+                if plan.small_variant is not None:
+                    small = Kernel(plan.small_plan) if plan.small_plan is not None else None
+                    k._attach_small(plan.variant.small_n, plan.small_variant, small)
                 _kernels[key] = k
     return k
 

@@ -428,3 +428,27 @@ def test_batch_entry_variants_bit_exact(name, bptrs, bvec):
     Batch(kern, bases, pitches, ns, stream).launch(stream)
     for env in envs:
         _check(case, env_to_host(env), want)
+
+
+@pytest.mark.parametrize("name", ["c1_dtg", "c2_maxwell", "c3_christoffel", "p2", "p3"])
+def test_size_classes_bitwise_at_the_boundary(name):
+    # launches of <= small_n points run Variant.small_class() (a hoisted
+    # second cubin for light kernels, 1 point/thread for heavier ones);
+    # both sides of the boundary must be bit-identical to the oracle
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.evaluator import kernel_for
+
+    prog, vs = tb.load(tb.PROGRAMS[name])
+    targets = [v.stmt.lhs.field for v in vs]
+    env = tb.make_env(prog, targets[0], 8, 0xC0FFEE)
+    kern = kernel_for(vs, env)
+    assert kern.small_n > 0
+    if kern.plan.variant.vec == 1:
+        assert kern.small is not None and kern.small.plan.variant.hoist
+    for n in (kern.small_n - 1, kern.small_n, kern.small_n + 3):
+        env = tb.make_env(prog, targets[0], n, 0xC0FFEE)
+        host = {k: f.data.cpu().numpy().copy() for k, f in env.items()}
+        eval_program(vs, env)
+        numpy_eval.eval_program(vs, host)
+        for t in targets:
+            assert same_bits(env[t].data.cpu().numpy(), host[t]), (n, t)
