@@ -70,7 +70,11 @@ int tlb_device_sm_count(int* out);
  * instead; after a successful compile the cubin is written there atomically.
  * The module is loaded lazily, per CUDA context, at first launch, so
  * compiling needs no GPU.  The source must define the four entry points
- * tlk_flat_v1, tlk_flat_v2, tlk_batch_v1, tlk_batch_v2 (see lowering.py). */
+ * tlk_flat_v1, tlk_flat_v2, tlk_batch_v1, tlk_batch_v2 (see lowering.py),
+ * and may define the TMA-staged tlk_stage_v1; the launch geometry is read
+ * from its `#define`s: TLK_THREADS (block size of the plain entries, default
+ * 256) and, for the staged entry, TLK_STAGE_THREADS (its block = tile, in
+ * points) and TLK_NSTAGE x TLK_NREAD tiles of dynamic shared memory. */
 int tlb_compile(const char* src, const char* const* opts, int nopts,
                 const char* cache_path, tlb_kernel** out);
 /* Compile log (warnings) of the last compile of `k` (empty when cached). */
@@ -95,9 +99,11 @@ int tlb_kernel_attrs(tlb_kernel* k, const char* entry, int* regs, int* local_byt
 /* One fused launch over points [0, n) of one grid.  field_bases[f] is the
  * device address of component 0 of field f, components `pitches[f]` doubles
  * apart.  vec: 0 = choose (2-point 128-bit path when every slot is 16-byte
- * aligned), 1 or 2 = force.  threads: block size (0 = 256; must not exceed
- * the TLK_THREADS the kernel was compiled with).  max_blocks: grid cap
- * (0 = one full wave at occupancy, -w = w waves).  Asynchronous on `stream`. */
+ * aligned), 1 or 2 = force, 3 = the TMA-staged entry (modules lowered with a staged variant;
+ * falls back to the 1-point entry when a slot is not 16-byte aligned).
+ * threads: block size (0 = the kernel's compiled TLK_THREADS; must not
+ * exceed it).  max_blocks: grid cap (0 = one full wave at occupancy, -w = w
+ * waves).  Asynchronous on `stream`. */
 int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
                const long long* pitches, int vec, int threads, long long max_blocks,
                void* stream);

@@ -68,6 +68,7 @@ struct Driver {
   CUresult (*ModuleLoadData)(CUmodule*, const void*) = nullptr;
   CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
   CUresult (*FuncGetAttribute)(int*, CUfunction_attribute, CUfunction) = nullptr;
+  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, unsigned, CUstream, void**, void**) = nullptr;
   CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
@@ -152,6 +153,7 @@ int load_driver_locked() {
             bind(h, g_cu.ModuleLoadData, "cuModuleLoadData") &&
             bind(h, g_cu.ModuleGetFunction, "cuModuleGetFunction") &&
             bind(h, g_cu.FuncGetAttribute, "cuFuncGetAttribute") &&
+            bind(h, g_cu.FuncSetAttribute, "cuFuncSetAttribute") &&
             bind(h, g_cu.LaunchKernel, "cuLaunchKernel") &&
             bind(h, g_cu.OccupancyMaxActiveBlocksPerMultiprocessor,
                  "cuOccupancyMaxActiveBlocksPerMultiprocessor") &&
@@ -233,17 +235,17 @@ int ctx_state(CUcontext ctx, CtxState** out) {
 
 // ---------------------------------------------------------------- kernel ----
 
-enum Entry { FLAT_V1 = 0, FLAT_V2, BATCH_V1, BATCH_V2, N_ENTRIES };
+// STAGE_V1 (the TMA-staged entry) exists only in modules lowered with a
+// staged variant; the others are in every module
+enum Entry { FLAT_V1 = 0, FLAT_V2, BATCH_V1, BATCH_V2, STAGE_V1, N_ENTRIES };
 const char* kEntryNames[N_ENTRIES] = {"tlk_flat_v1", "tlk_flat_v2", "tlk_batch_v1",
-                                      "tlk_batch_v2"};
+                                      "tlk_batch_v2", "tlk_stage_v1"};
 
 struct Loaded {
   CUmodule mod = nullptr;
   CUfunction fn[N_ENTRIES] = {};
-  int occ[N_ENTRIES] = {};  // resident blocks per SM at kDefaultThreads
+  int occ[N_ENTRIES] = {};  // resident blocks per SM at the kernel's block size
 };
-
-constexpr int kDefaultThreads = 256;
 
 }  // namespace
 
@@ -254,6 +256,9 @@ struct tlb_kernel {
   std::vector<int> slot_field;
   std::vector<long long> slot_comp;
   std::vector<int> slot_flags;
+  int threads = 256;   // compiled TLK_THREADS: default block size (from the source)
+  int stage_threads = 0;  // block size (= tile) of tlk_stage_v1 (from the source)
+  int stage_smem = 0;     // its dynamic shared memory (from the source)
   std::mutex mu;
   std::map<CUcontext, Loaded> loaded;
 };
@@ -279,8 +284,21 @@ int load_module(tlb_kernel* k, CUcontext ctx, Loaded** out) {
   Loaded L;
   CU(g_cu.ModuleLoadData(&L.mod, k->cubin.data()), "cuModuleLoadData");
   for (int e = 0; e < N_ENTRIES; ++e) {
-    CU(g_cu.ModuleGetFunction(&L.fn[e], L.mod, kEntryNames[e]), kEntryNames[e]);
-    CU(g_cu.OccupancyMaxActiveBlocksPerMultiprocessor(&L.occ[e], L.fn[e], kDefaultThreads, 0),
+    if (e == STAGE_V1) {
+      if (k->stage_smem <= 0 ||
+          g_cu.ModuleGetFunction(&L.fn[e], L.mod, kEntryNames[e]) != CUDA_SUCCESS) {
+        L.fn[e] = nullptr;
+        continue;
+      }
+      CU(g_cu.FuncSetAttribute(L.fn[e], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                               k->stage_smem),
+         "cuFuncSetAttribute(stage smem)");
+    } else {
+      CU(g_cu.ModuleGetFunction(&L.fn[e], L.mod, kEntryNames[e]), kEntryNames[e]);
+    }
+    CU(g_cu.OccupancyMaxActiveBlocksPerMultiprocessor(
+           &L.occ[e], L.fn[e], e == STAGE_V1 ? k->stage_threads : k->threads,
+           e == STAGE_V1 ? k->stage_smem : 0),
        "cuOccupancyMaxActiveBlocksPerMultiprocessor");
     if (L.occ[e] < 1) L.occ[e] = 1;
   }
@@ -361,10 +379,33 @@ int tlb_device_sm_count(int* out) {
   return 0;
 }
 
+// Value of `#define NAME <int>` in a generated source (lowering.py writes the
+// launch geometry there), or `dflt`.
+long long source_define(const char* src, const char* name, long long dflt) {
+  const std::string key = std::string("#define ") + name + " ";
+  const char* p = strstr(src, key.c_str());
+  return p ? atoll(p + key.size()) : dflt;
+}
+
 int tlb_compile(const char* src, const char* const* opts, int nopts, const char* cache_path,
                 tlb_kernel** out) {
   if (!src || !out) return fail("tlb_compile: null argument");
   std::unique_ptr<tlb_kernel> k(new tlb_kernel);
+  // launch geometry from the source: block size, and the staged entry's
+  // tile ring (TLK_NSTAGE x TLK_NREAD x TLK_THREADS doubles)
+  k->threads = (int)source_define(src, "TLK_THREADS", 256);
+  const long long nstage = source_define(src, "TLK_NSTAGE", 0);
+  if (k->threads < 32 || k->threads > 1024 || k->threads % 32)
+    return fail("tlb_compile: TLK_THREADS %d is not a block size", k->threads);
+  if (nstage > 0) {
+    k->stage_threads = (int)source_define(src, "TLK_STAGE_THREADS", 128);
+    if (k->stage_threads < 32 || k->stage_threads > 1024 || k->stage_threads % 32)
+      return fail("tlb_compile: TLK_STAGE_THREADS %d is not a block size", k->stage_threads);
+    const long long smem =
+        nstage * source_define(src, "TLK_NREAD", 1) * k->stage_threads * 8;
+    if (smem > 227 * 1024) return fail("tlb_compile: staged tile ring of %lld bytes", smem);
+    k->stage_smem = (int)smem;
+  }
   if (file_exists(cache_path) && read_file(cache_path, &k->cubin)) {
     *out = k.release();
     return 0;
@@ -435,6 +476,7 @@ int tlb_kernel_attrs(tlb_kernel* k, const char* entry, int* regs, int* local_byt
   if (load_module(k, ctx, &L)) return 1;
   for (int e = 0; e < N_ENTRIES; ++e) {
     if (strcmp(entry, kEntryNames[e])) continue;
+    if (!L->fn[e]) return fail("tlb_kernel_attrs: entry %s not in this module", entry);
     CU(g_cu.FuncGetAttribute(regs, CU_FUNC_ATTRIBUTE_NUM_REGS, L->fn[e]), "attr regs");
     CU(g_cu.FuncGetAttribute(local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, L->fn[e]),
        "attr local");
@@ -448,20 +490,34 @@ int tlb_kernel_attrs(tlb_kernel* k, const char* entry, int* regs, int* local_byt
 namespace {
 
 int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n, const uint64_t* slots,
-                bool vec2, int threads, long long max_blocks, CUstream stream) {
+                bool vec2, int threads, long long max_blocks, CUstream stream,
+                bool stage = false) {
   const size_t m = k->slot_field.size();
   // parameter block: { long long n; double* p[m]; } — passed by value
   std::vector<uint64_t> param(1 + m);
   param[0] = (uint64_t)n;
   memcpy(&param[1], slots, m * sizeof(uint64_t));
+  if (threads <= 0) threads = k->threads;
+  if (stage) {
+    // persistent: one block per resident slot, each walks whole tiles; the
+    // block is the tile (the compiled TLK_STAGE_THREADS)
+    threads = k->stage_threads;
+    long long tiles = std::max(1LL, n / threads);
+    long long blocks = std::min<long long>(tiles, (long long)st->sm_count * L->occ[STAGE_V1]);
+    if (max_blocks > 0) blocks = std::min(blocks, max_blocks);
+    void* args[] = {param.data()};
+    CU(g_cu.LaunchKernel(L->fn[STAGE_V1], (unsigned)blocks, 1, 1, (unsigned)threads, 1, 1,
+                         (unsigned)k->stage_smem, stream, args, nullptr),
+       "cuLaunchKernel(stage)");
+    return 0;
+  }
   const int e = vec2 ? FLAT_V2 : FLAT_V1;
-  if (threads <= 0) threads = kDefaultThreads;
   long long units = vec2 ? n / 2 : n;
   if (units < 1) units = 1;
   long long blocks = (units + threads - 1) / threads;
   // max_blocks > 0: explicit cap; 0: one full wave at occupancy; -w: w waves
   int occ = L->occ[e];
-  if (threads != kDefaultThreads) {
+  if (threads != k->threads) {
     g_cu.OccupancyMaxActiveBlocksPerMultiprocessor(&occ, L->fn[e], threads, 0);
     occ = std::max(occ, 1);
   }
@@ -493,6 +549,15 @@ int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
   std::vector<uint64_t> slots(k->slot_field.size());
   bool al;
   if (resolve_slots(k, field_bases, pitches, slots.data(), &al)) return 1;
+  if (vec == 3) {
+    // TMA-staged entry: bulk copies need 16-byte aligned sources (its block
+    // size is the compiled tile; `threads` applies to the plain entries)
+    if (!L->fn[STAGE_V1]) return fail("tlb_launch: vec=3 but the module has no staged entry");
+    if (al)
+      return launch_flat(k, L, st, n, slots.data(), false, threads, max_blocks,
+                         (CUstream)stream, true);
+    vec = 1;  // unaligned slab view: the plain 1-point entry (same results)
+  }
   bool vec2 = vec == 2 ? true : (vec == 1 ? false : al);
   if (vec2 && !al) return fail("tlb_launch: vec=2 requested but a slot is not 16-byte aligned");
   return launch_flat(k, L, st, n, slots.data(), vec2, threads, max_blocks, (CUstream)stream);
@@ -545,7 +610,7 @@ int tlb_batch_launch(tlb_batch* b, int vec, int threads, void* stream) {
   if (load_module(b->k, ctx, &L)) return 1;
   const bool v2 = b->vec2 && vec != 1;
   const int e = v2 ? BATCH_V2 : BATCH_V1;
-  if (threads <= 0) threads = kDefaultThreads;
+  if (threads <= 0) threads = b->k->threads;
   long long units = v2 ? (b->max_n + 1) / 2 : b->max_n;
   long long gx = std::max(1LL, (units + threads - 1) / threads);
   long long gy = std::min<long long>(b->ndom, 65535);

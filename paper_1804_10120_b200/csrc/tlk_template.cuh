@@ -9,7 +9,7 @@
 //   * T = double  (one point per thread step) or
 //     T = double2 (two consecutive points: 128-bit LDG/STG per component);
 //   * streaming loads/stores (evict-first: every byte is touched once);
-//   * four entry points:
+//   * four entry points (plus the opt-in TMA-staged tlk_stage_v1 at the end):
 //       tlk_flat_v1 / tlk_flat_v2   one grid, per-slot base pointers passed
 //                                   by value in the parameter block (constant
 //                                   bank) — no device pointer arrays, which
@@ -27,8 +27,8 @@
 //
 // lowering.py prepends `#define TLK_NSLOTS <number of pointer slots>` and
 // replaces the @@TLK_BODY@@ marker line below with the per-point body
-// `template <typename T, typename P> tlk_point(const P& P_, long long x)`,
-// which addresses slot j as `P_.p[j] + x`.
+// `template <typename T, int LD, typename P> tlk_point(const P& P_, long long x)`,
+// which addresses slot j as `P_.p[j] + x` and loads with tl_ld<T, LD>.
 
 #ifndef TLK_THREADS
 #define TLK_THREADS 256
@@ -68,6 +68,8 @@ template <> __device__ __forceinline__ double2 tl_splat<double2>(double c) { ret
 //            1: ld.global.nc.L1::no_allocate as a movable asm (the lowering
 //               only selects it when no slot is both read and written)
 //            2: plain ld.global
+//            3: plain dereference (only as tl_ld<T, 3>: the staged entry's
+//               shared-memory tiles, LDS)
 #ifndef TLK_LDMODE
 #define TLK_LDMODE 0
 #endif
@@ -77,30 +79,31 @@ template <> __device__ __forceinline__ double2 tl_splat<double2>(double c) { ret
 #define TLK_STMODE 0
 #endif
 
-template <typename T> __device__ __forceinline__ T tl_ld(const double* p);
-// TLK_LDMODE 3 (staged entry): plain dereference, so reads of the shared-
-// memory tiles compile to LDS and the global tail path to LDG
-template <> __device__ __forceinline__ double tl_ld<double>(const double* p) {
-#if TLK_LDMODE == 0
-  return __ldcs(p);
-#elif TLK_LDMODE == 1
-  double v;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-#else
-  return *p;
-#endif
-}
-template <> __device__ __forceinline__ double2 tl_ld<double2>(const double* p) {
-#if TLK_LDMODE == 0
-  return __ldcs(reinterpret_cast<const double2*>(p));
-#elif TLK_LDMODE == 1
-  double2 v;
-  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-#else
-  return *reinterpret_cast<const double2*>(p);
-#endif
+// LD is a template parameter so one module can hold entries with different
+// load flavours (the staged entry reads its tiles with mode 3).
+template <typename T, int LD = TLK_LDMODE>
+__device__ __forceinline__ T tl_ld(const double* p) {
+  if constexpr (sizeof(T) == sizeof(double)) {
+    if constexpr (LD == 0) {
+      return __ldcs(p);
+    } else if constexpr (LD == 1) {
+      double v;
+      asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+      return v;
+    } else {
+      return *p;
+    }
+  } else {
+    if constexpr (LD == 0) {
+      return __ldcs(reinterpret_cast<const double2*>(p));
+    } else if constexpr (LD == 1) {
+      double2 v;
+      asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+      return v;
+    } else {
+      return *reinterpret_cast<const double2*>(p);
+    }
+  }
 }
 
 __device__ __forceinline__ void tl_st(double* p, double v) {
@@ -218,25 +221,26 @@ tlk_batch_v2(const long long* __restrict__ table, int ndom) {
 }
 
 // ------------------------------------------------ TMA-staged entry (opt-in)
-// tlk_stage_v1: persistent blocks walk tiles of TLK_THREADS points; for each
+// tlk_stage_v1: persistent blocks walk tiles of TLK_STAGE_THREADS points (one
+// per thread; its own block size and launch bounds); for each
 // tile one elected thread issues one 1-D bulk copy (cp.async.bulk, the TMA
 // engine) per read slot into a TLK_NSTAGE-deep shared-memory ring, completion
 // tracked by an mbarrier (complete_tx); every thread then runs the per-point
 // body with its read slots pointing into the tile and its write slots at the
 // global arrays.  The copies of the next TLK_NSTAGE-1 tiles are in flight
 // while a tile computes.  Points past the last whole tile take the plain
-// path.  Compiled only when the lowering defines TLK_NSTAGE (with TLK_NREAD
-// and the per-slot read ordinals TLK_RORD); needs every read slot 16-byte
-// aligned (the runtime checks).
+// path.  Compiled only when the lowering defines TLK_NSTAGE (with TLK_NREAD,
+// TLK_STAGE_THREADS and the per-slot read ordinals TLK_RORD); needs every
+// read slot 16-byte aligned (the runtime checks).
 #ifdef TLK_NSTAGE
 __device__ __forceinline__ unsigned tlk_smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
 
-extern "C" __global__ void __launch_bounds__(TLK_THREADS)
+extern "C" __global__ void __launch_bounds__(TLK_STAGE_THREADS)
 tlk_stage_v1(const tlk_flat_params prm) {
   constexpr int kRord[TLK_NSLOTS] = TLK_RORD;
-  constexpr int kTile = TLK_THREADS;
+  constexpr int kTile = TLK_STAGE_THREADS;
   extern __shared__ __align__(128) double tlk_sm[];  // [NSTAGE][NREAD][kTile]
   __shared__ __align__(8) unsigned long long bar[TLK_NSTAGE];
   const long long ntiles = prm.n / kTile;
@@ -283,7 +287,7 @@ tlk_stage_v1(const tlk_flat_params prm) {
     for (int j = 0; j < TLK_NSLOTS; ++j)
       q.p[j] = kRord[j] >= 0 ? tlk_sm + ((long long)s * TLK_NREAD + kRord[j]) * kTile
                              : prm.p[j] + t * kTile;
-    tlk_point<double>(q, tid);
+    tlk_point<double, 3>(q, tid);
     __syncthreads();  // every thread is done with stage s
     if (tid == 0) {
       const long long tn = t + (long long)TLK_NSTAGE * gridDim.x;

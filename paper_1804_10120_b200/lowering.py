@@ -389,11 +389,11 @@ def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = F
         params = ", ".join(
             ("double* __restrict__" if slot_flags[j] & SLOT_WRITE else
              "const double* __restrict__") + f" p{j}" for j in range(nslots))
-        out = ["template <typename T>",
+        out = ["template <typename T, int LD = TLK_LDMODE>",
                f"__device__ __forceinline__ void tlk_body(const long long x, {params}) {{"]
         ptr = "p{}".format
     else:
-        out = ["template <typename T, typename P>",
+        out = ["template <typename T, int LD = TLK_LDMODE, typename P>",
                "__device__ __forceinline__ void tlk_point(const P& P_, const long long x) {"]
         ptr = "P_.p[{}]".format
     if hoist_loads:
@@ -403,7 +403,7 @@ def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = F
         last = {ins.slot: k for k, ins in enumerate(instrs) if ins.op == "st"}
     for k, ins in enumerate(instrs):
         if ins.op == "ld":
-            out.append(f"  const T v{ins.dst} = tl_ld<T>({ptr(ins.slot)} + x);")
+            out.append(f"  const T v{ins.dst} = tl_ld<T, LD>({ptr(ins.slot)} + x);")
         elif ins.op == "st":
             if last[ins.slot] != k:
                 continue
@@ -422,9 +422,9 @@ def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = F
     out.append("}")
     if restrict:
         args = ", ".join(f"P_.p[{j}]" for j in range(nslots))
-        out += ["template <typename T, typename P>",
+        out += ["template <typename T, int LD = TLK_LDMODE, typename P>",
                 "__device__ __forceinline__ void tlk_point(const P& P_, const long long x) {",
-                f"  tlk_body<T>(x, {args});", "}"]
+                f"  tlk_body<T, LD>(x, {args});", "}"]
     return out
 
 
@@ -460,11 +460,16 @@ class Variant:
     batch_vec: int = 1  # points per thread of the multi-domain batch entry
     batch_ptrs: int = 0  # TLK_BATCH_PTRS: 0 shared-memory staging, 1 direct table reads
     small_n: int = 0  # launches of <= small_n points run small_class() (0: never)
+    stage: int = 0  # >0: TMA-staged entry tlk_stage_v1 with a `stage`-deep tile ring
+    threads: int = 256  # TLK_THREADS: block size of the flat and batch entries
+    stage_threads: int = 128  # TLK_STAGE_THREADS: the staged entry's block = tile (points)
 
     def tag(self) -> str:
         t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
              f"v{self.vec}w{self.waves}b{self.batch_vec}{self.batch_ptrs}")
-        return t + (f"s{self.small_n.bit_length() - 1}" if self.small_n else "")
+        t += f"s{self.small_n.bit_length() - 1}" if self.small_n else ""
+        t += f"g{self.stage}x{self.stage_threads}" if self.stage else ""
+        return t + (f"n{self.threads}" if self.threads != 256 else "")
 
     def small_class(self) -> "Variant":
         """Choices for launches of at most ``small_n`` points, where a
@@ -479,15 +484,17 @@ class Variant:
           time choice, same cubin): twice the threads in flight — C3 at
           128^3 +3 %, P3 +5 %, P2 +4 % at 2^20; the 2-point body wins
           again from 2^23 points."""
-        if self.vec == 1:
+        if self.vec == 1 and not self.stage:
             return Variant(**{**self.__dict__, "hoist": True, "small_n": 0})
         return Variant(**{**self.__dict__, "vec": 1, "waves": 4, "small_n": 0})
 
     def same_code(self, other: "Variant") -> bool:
         """Whether two variants compile to the same cubin (vec/waves are
         launch-time choices; both entry points are in every module)."""
-        return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs)
-                == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs))
+        return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs, self.stage,
+                 self.threads, self.stage_threads)
+                == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs, other.stage,
+                    other.threads, other.stage_threads))
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -511,17 +518,44 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
     * the multi-domain batch entry always runs one point per thread with the
       domain's slot pointers staged in shared memory (small 16^3 domains:
       twice the blocks in flight hide the per-domain pointer fetch; C4 P2
-      5.64 -> 6.10 TB/s, P3 chain 5.10 -> 5.87 TB/s, profiles/r01/tune_batch.jsonl).
+      5.64 -> 6.10 TB/s, P3 chain 5.10 -> 5.87 TB/s, profiles/r01/tune_batch.jsonl);
+    * above the small-N class, read-only-input programs run the TMA-staged
+      entry (tlk_stage_v1: one bulk copy per read slot per tile into a
+      3-deep shared-memory ring) when that ring leaves room for two blocks
+      per SM, or when statements chain (the plain P3 body holds too many
+      registers to keep its loads in flight): C1 +5-7 %, Maxwell +3-4 %,
+      C3 +1-3 %, P3 +3-10 % over the plain entries at 2^24-2^26
+      (profiles/r01/tune_stage*.jsonl).  P2 (40 reads: one block per SM)
+      stays on the plain entry, which holds more bytes in flight.
     """
     arrays = reads + writes
+
+    def ring_tile(tiles) -> int:
+        # largest tile whose 3-deep ring leaves room for two blocks per SM
+        for t in tiles:
+            if 3 * reads * t * 8 <= STAGE_RING_2CTA:
+                return t
+        return 0
+
     if n_ops <= 1.5 * arrays:
-        return Variant(restrict=True, hoist=False, ldmode=0, vec=1, waves=4,
-                       small_n=SMALL_N_LIGHT)
+        tile = ring_tile((256, 128)) if rw_slots == 0 else 0
+        return Variant(restrict=True, hoist=tile > 0, ldmode=0, vec=1, waves=4,
+                       small_n=SMALL_N_LIGHT, stage=3 if tile else 0, stage_threads=tile or 128)
     if rw_slots == 0:
+        tile = 128 if chained else ring_tile((128,))
         return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=2, waves=4 if chained else 1,
-                       small_n=SMALL_N_HEAVY)
+                       small_n=SMALL_N_HEAVY, stage=3 if tile else 0, stage_threads=tile or 128)
     return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
 
+
+# dynamic shared memory budget of the staged entry's tile ring (bytes; the
+# 227 KB per-block maximum less room for the static mbarriers)
+STAGE_SMEM_MAX = 224 * 1024
+# ring size that still lets two staged blocks share an SM (the policy stages
+# a non-chained program only then: with one block the ring holds too few
+# bytes in flight — P2, 40 reads: 97.9 % vs 99.1 % unstaged at 2^28,
+# profiles/r01/bench_stage_ab/)
+STAGE_RING_2CTA = 112 * 1024
 
 # size classes (Variant.small_class): largest launch, in points, that still
 # runs the small-N choices — the crossovers in profiles/r01/tune_cross.jsonl
@@ -547,6 +581,12 @@ def _env_variant(v: Variant) -> Variant:
         kw["batch_vec"] = int(env["TLK_BATCH_VEC"])
     if "TLK_BATCH_PTRS" in env:
         kw["batch_ptrs"] = int(env["TLK_BATCH_PTRS"])
+    if "TLK_STAGE" in env:
+        kw["stage"] = int(env["TLK_STAGE"])
+    if "TLK_THREADS" in env:
+        kw["threads"] = int(env["TLK_THREADS"])
+    if "TLK_STAGE_THREADS" in env:
+        kw["stage_threads"] = int(env["TLK_STAGE_THREADS"])
     if kw:
         kw["small_n"] = 0  # a forced variant applies at every size ...
     if "TLK_SMALL_N" in env:
@@ -593,12 +633,39 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         variant = Variant(**{**variant.__dict__, "hoist": hoist_loads})
     if variant.ldmode == 1 and rw:
         variant = Variant(**{**variant.__dict__, "ldmode": 0})  # see Variant docstring
+    if variant.stage and rw:
+        # a staged read-modify-write slot would be stored into its own tile
+        variant = Variant(**{**variant.__dict__, "stage": 0})
+    if variant.stage:
+        # the tile ring must fit the 227 KB a block can hold: shallower ring,
+        # then smaller tiles; below two stages nothing overlaps, so the plain
+        # entries are used instead
+        tile = variant.stage_threads
+        depth = min(variant.stage, STAGE_SMEM_MAX // (8 * tile * max(reads, 1)))
+        while depth < 2 and tile > 32:
+            tile //= 2
+            depth = min(variant.stage, STAGE_SMEM_MAX // (8 * tile * max(reads, 1)))
+        if (depth, tile) != (variant.stage, variant.stage_threads):
+            variant = Variant(**{**variant.__dict__, "stage": depth if depth >= 2 else 0,
+                                 "stage_threads": tile})
     body = "\n".join(_emit_body(b.instrs, b.slot_flags, variant.hoist, variant.restrict))
     header = [f"// generated by paper_1804_10120_b200.lowering ({LOWERING_VERSION})",
               f"// variant {variant.tag()}"]
     for v in statements:
         header.append("// " + _statement_comment(v))
     header.append(f"#define TLK_NSLOTS {n_slots}")
+    header.append(f"#define TLK_THREADS {variant.threads}")
+    if variant.stage:
+        # TMA-staged entry: read slots come from shared-memory tiles
+        # (tlk_point<double, 3>: plain dereferences, LDS)
+        rord, r = [], 0
+        for fl in b.slot_flags:
+            rord.append(r if fl & SLOT_READ else -1)
+            r += 1 if fl & SLOT_READ else 0
+        header.append(f"#define TLK_NSTAGE {variant.stage}")
+        header.append(f"#define TLK_NREAD {max(r, 1)}")
+        header.append(f"#define TLK_STAGE_THREADS {variant.stage_threads}")
+        header.append("#define TLK_RORD {" + ",".join(map(str, rord)) + "}")
     header.append(f"#define TLK_LDMODE {variant.ldmode}")
     header.append(f"#define TLK_BATCH_PTRS {variant.batch_ptrs}")
     src = "\n".join(header) + "\n" + template_text().replace("// @@TLK_BODY@@", body)

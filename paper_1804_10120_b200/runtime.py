@@ -33,7 +33,8 @@ BASE_OPTIONS = (
 EXPORTED = (
     "tlb_abi_version", "tlb_init", "tlb_last_error", "tlb_nvrtc_version", "tlb_device_sm_count",
     "tlb_compile", "tlb_kernel_log", "tlb_kernel_cubin", "tlb_kernel_destroy",
-    "tlb_kernel_set_slots", "tlb_kernel_attrs", "tlb_launch", "tlb_batch_create",
+    "tlb_kernel_set_slots", "tlb_kernel_attrs", "tlb_launch",
+    "tlb_batch_create",
     "tlb_batch_launch", "tlb_batch_destroy", "tlb_exec_host", "tlb_fill_uniform",
     "tlb_harness_call", "tlb_release_staging",
 )
@@ -111,18 +112,9 @@ def nvrtc_version() -> tuple[int, int]:
     return a.value, b.value
 
 
-def launch_config() -> tuple[int, int]:
-    """(threads per block, grid cap) for launches: TLK_THREADS (default 256,
-    also the kernels' __launch_bounds__); the number of waves comes from the
-    plan's Variant (lowering.choose_variant / TLK_WAVES)."""
-    threads = int(os.environ.get("TLK_THREADS", "256"))
-    return threads, 0
-
-
 def compile_options() -> list[str]:
+    # the block size (TLK_THREADS) is part of the source: lowering.Variant.threads
     opts = list(BASE_OPTIONS)
-    threads = int(os.environ.get("TLK_THREADS", "256"))
-    opts.append(f"-DTLK_THREADS={threads}")
     extra = os.environ.get("TLK_DEFINES", "").split()
     opts += extra
     return opts
@@ -166,10 +158,16 @@ class Kernel:
                                      _arr(c_int, plan.slot_flags)), "tlb_kernel_set_slots")
         self.nfields = len(plan.fields)
         self.launches = 0
-        self.threads, self.max_blocks = launch_config()
         var = plan.variant
-        # vec 2 = auto (128-bit when every slot is 16-byte aligned), 1 = forced scalar
+        # block size = the compiled TLK_THREADS; grid = one wave unless the
+        # variant asks for more (lowering.choose_variant / TLK_WAVES)
+        self.threads = var.threads if var is not None else 256
+        self.max_blocks = 0
+        # vec 2 = auto (128-bit when every slot is 16-byte aligned), 1 = forced
+        # scalar, 3 = the TMA-staged entry
         self.vec = 1 if (var is not None and var.vec == 1) else 0
+        if var is not None and var.stage:
+            self.vec = 3  # the staged entry (its tile ring size is read from the source)
         if var is not None and var.waves > 1 and self.max_blocks == 0:
             self.max_blocks = -var.waves
         self.batch_vec = 1 if (var is not None and var.batch_vec == 1) else 0

@@ -285,7 +285,8 @@ def test_fuzzed_programs_match_oracle(seed):
 
 
 VARIANTS = [dict(restrict=False), dict(hoist=True), dict(vec=1), dict(ldmode=1),
-            dict(hoist=True, ldmode=1, vec=1), dict(waves=4)]
+            dict(hoist=True, ldmode=1, vec=1), dict(waves=4), dict(stage=2),
+            dict(stage=3, hoist=True)]
 
 
 @pytest.mark.parametrize("vkw", VARIANTS, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()))
@@ -443,7 +444,11 @@ def test_size_classes_bitwise_at_the_boundary(name):
     env = tb.make_env(prog, targets[0], 8, 0xC0FFEE)
     kern = kernel_for(vs, env)
     assert kern.small_n > 0
-    if kern.plan.variant.vec == 1:
+    var = kern.plan.variant
+    if var.stage:
+        # staged above small_n, the same cubin's 1-point entry below
+        assert kern.vec == 3 and kern.small is None and kern.small_vec == 1
+    elif var.vec == 1:
         assert kern.small is not None and kern.small.plan.variant.hoist
     for n in (kern.small_n - 1, kern.small_n, kern.small_n + 3):
         env = tb.make_env(prog, targets[0], n, 0xC0FFEE)
@@ -452,3 +457,34 @@ def test_size_classes_bitwise_at_the_boundary(name):
         numpy_eval.eval_program(vs, host)
         for t in targets:
             assert same_bits(env[t].data.cpu().numpy(), host[t]), (n, t)
+
+
+@pytest.mark.parametrize("name", ["c1_dtg", "c2_maxwell", "c3_christoffel", "p2", "p3"])
+@pytest.mark.parametrize("stage", [2, 4])
+def test_tma_staged_entry_bitwise(name, stage):
+    # many whole tiles per block (ring wrap-around, mbarrier phase flips), a
+    # ragged tail, and an unaligned slab view (falls back to the plain entry)
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.evaluator import _bind
+    from paper_1804_10120_b200.lowering import Variant, lower_program
+    from paper_1804_10120_b200.runtime import Kernel
+
+    prog, vs = tb.load(tb.PROGRAMS[name])
+    targets = [v.stmt.lhs.field for v in vs]
+    for n, lo in ((256 * 148 * 2 * 7 + 77, 0), (300001, 0), (300001, 1), (255, 0)):
+        env = tb.make_env(prog, targets[0], n, 0xC0FFEE)
+        host = {k: f.data.cpu().numpy().copy() for k, f in env.items()}
+        _, _, stores = _bind(vs, env)
+        plan = lower_program(vs, variant=Variant(stage=stage))
+        if plan.variant.stage == 0:
+            pytest.skip("read-modify-write program: no staged entry")
+        k = Kernel(plan)
+        assert k.vec == 3
+        k.launch(n - lo, [s.base + 8 * lo for s in stores], [s.pitch for s in stores],
+                 torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        sub = {key: a[..., lo:] for key, a in host.items()}
+        numpy_eval.eval_program(vs, sub)
+        for t in targets:
+            got = env[t].data.cpu().numpy()[..., lo:]
+            assert same_bits(got, sub[t]), (n, lo, t)
