@@ -218,6 +218,13 @@ def build_p2_env(n_local: int, lo: int, device: str):
 # ------------------------------------------------------------ our impl --
 
 
+def entry_name(kern, n: int) -> str:
+    """The entry point a launch of n points takes (runtime.Kernel.launch)."""
+    if n <= kern.small_n:
+        return "tlk_flat_v1"
+    return {3: "tlk_stage_v1", 1: "tlk_flat_v1"}.get(kern.vec, "tlk_flat_v2")
+
+
 def run_ours(args, dist: Dist) -> dict | None:
     import torch
 
@@ -329,7 +336,7 @@ def run_ours(args, dist: Dist) -> dict | None:
             "frac": achieved / peak,
             "traffic": traffic,
             "peak_source": peak_src,
-            "kernel": "tlk_flat_v2 (fused P2)",
+            "kernel": f"{entry_name(kern, n_local)} (fused P2, variant {plan.variant.tag()})",
             "kernel_ms": kernel_ms,
             "kernel_ms_max_over_ranks": kernel_ms_max,
             "algorithmic_bytes_per_launch": alg_bytes,
