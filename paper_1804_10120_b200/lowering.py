@@ -364,7 +364,7 @@ def _operand(x) -> str:
 
 
 def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = False,
-               restrict: bool = True) -> list[str]:
+               restrict: bool = True, direct: set[int] | frozenset = frozenset()) -> list[str]:
     """C++ text of the per-point body.
 
     With ``restrict`` (default) the body is a function of one
@@ -403,7 +403,10 @@ def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = F
         last = {ins.slot: k for k, ins in enumerate(instrs) if ins.op == "st"}
     for k, ins in enumerate(instrs):
         if ins.op == "ld":
-            out.append(f"  const T v{ins.dst} = tl_ld<T, LD>({ptr(ins.slot)} + x);")
+            # `direct` slots bypass the staged entry's ring: under LD 3 they
+            # still load from global memory
+            ld = "(LD == 3 ? 1 : LD)" if ins.slot in direct else "LD"
+            out.append(f"  const T v{ins.dst} = tl_ld<T, {ld}>({ptr(ins.slot)} + x);")
         elif ins.op == "st":
             if last[ins.slot] != k:
                 continue
@@ -463,12 +466,14 @@ class Variant:
     stage: int = 0  # >0: TMA-staged entry tlk_stage_v1 with a `stage`-deep tile ring
     threads: int = 256  # TLK_THREADS: block size of the flat and batch entries
     stage_threads: int = 128  # TLK_STAGE_THREADS: the staged entry's block = tile (points)
+    stage_reads: int = 0  # read slots copied through the ring (0 = all; the rest load directly)
 
     def tag(self) -> str:
         t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
              f"v{self.vec}w{self.waves}b{self.batch_vec}{self.batch_ptrs}")
         t += f"s{self.small_n.bit_length() - 1}" if self.small_n else ""
         t += f"g{self.stage}x{self.stage_threads}" if self.stage else ""
+        t += f"r{self.stage_reads}" if self.stage and self.stage_reads else ""
         return t + (f"n{self.threads}" if self.threads != 256 else "")
 
     def small_class(self) -> "Variant":
@@ -492,9 +497,9 @@ class Variant:
         """Whether two variants compile to the same cubin (vec/waves are
         launch-time choices; both entry points are in every module)."""
         return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs, self.stage,
-                 self.threads, self.stage_threads)
+                 self.threads, self.stage_threads, self.stage_reads)
                 == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs, other.stage,
-                    other.threads, other.stage_threads))
+                    other.threads, other.stage_threads, other.stage_reads))
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -587,6 +592,8 @@ def _env_variant(v: Variant) -> Variant:
         kw["threads"] = int(env["TLK_THREADS"])
     if "TLK_STAGE_THREADS" in env:
         kw["stage_threads"] = int(env["TLK_STAGE_THREADS"])
+    if "TLK_STAGE_READS" in env:
+        kw["stage_reads"] = int(env["TLK_STAGE_READS"])
     if kw:
         kw["small_n"] = 0  # a forced variant applies at every size ...
     if "TLK_SMALL_N" in env:
@@ -629,6 +636,10 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     phases = _phases(b.instrs)
     if variant is None:
         variant = _env_variant(choose_variant(reads, writes, n_ops, rw, b.chained))
+        if "TLK_STAGE_FRAC" in os.environ:  # tuning: staged share of the read slots
+            frac = float(os.environ["TLK_STAGE_FRAC"])
+            variant = Variant(**{**variant.__dict__,
+                                 "stage_reads": max(1, round(frac * reads))})
     if hoist_loads is not None:
         variant = Variant(**{**variant.__dict__, "hoist": hoist_loads})
     if variant.ldmode == 1 and rw:
@@ -641,14 +652,29 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         # then smaller tiles; below two stages nothing overlaps, so the plain
         # entries are used instead
         tile = variant.stage_threads
-        depth = min(variant.stage, STAGE_SMEM_MAX // (8 * tile * max(reads, 1)))
+        staged = min(reads, variant.stage_reads) if variant.stage_reads else reads
+        depth = min(variant.stage, STAGE_SMEM_MAX // (8 * tile * max(staged, 1)))
         while depth < 2 and tile > 32:
             tile //= 2
-            depth = min(variant.stage, STAGE_SMEM_MAX // (8 * tile * max(reads, 1)))
+            depth = min(variant.stage, STAGE_SMEM_MAX // (8 * tile * max(staged, 1)))
         if (depth, tile) != (variant.stage, variant.stage_threads):
             variant = Variant(**{**variant.__dict__, "stage": depth if depth >= 2 else 0,
                                  "stage_threads": tile})
-    body = "\n".join(_emit_body(b.instrs, b.slot_flags, variant.hoist, variant.restrict))
+    rord: list[int] = []
+    if variant.stage:
+        # TMA-staged entry: the first `stage_reads` read slots (all by
+        # default) come through the shared-memory ring (tlk_point<double, 3>:
+        # plain dereferences, LDS); the others load straight from global
+        # memory (ld.global.nc: staged variants have no read-write slot)
+        cap = variant.stage_reads or n_slots
+        r = 0
+        for fl in b.slot_flags:
+            take = bool(fl & SLOT_READ) and r < cap
+            rord.append(r if take else -1)
+            r += 1 if take else 0
+    direct = {j for j, o in enumerate(rord) if o < 0 and b.slot_flags[j] & SLOT_READ}
+    body = "\n".join(_emit_body(b.instrs, b.slot_flags, variant.hoist, variant.restrict,
+                                direct))
     header = [f"// generated by paper_1804_10120_b200.lowering ({LOWERING_VERSION})",
               f"// variant {variant.tag()}"]
     for v in statements:
@@ -656,14 +682,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     header.append(f"#define TLK_NSLOTS {n_slots}")
     header.append(f"#define TLK_THREADS {variant.threads}")
     if variant.stage:
-        # TMA-staged entry: read slots come from shared-memory tiles
-        # (tlk_point<double, 3>: plain dereferences, LDS)
-        rord, r = [], 0
-        for fl in b.slot_flags:
-            rord.append(r if fl & SLOT_READ else -1)
-            r += 1 if fl & SLOT_READ else 0
         header.append(f"#define TLK_NSTAGE {variant.stage}")
-        header.append(f"#define TLK_NREAD {max(r, 1)}")
+        header.append(f"#define TLK_NREAD {max(len(rord) - rord.count(-1), 1)}")
         header.append(f"#define TLK_STAGE_THREADS {variant.stage_threads}")
         header.append("#define TLK_RORD {" + ",".join(map(str, rord)) + "}")
     header.append(f"#define TLK_LDMODE {variant.ldmode}")

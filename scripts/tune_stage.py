@@ -1,7 +1,7 @@
 """TMA-staged entry (tlk_stage_v1) against the policy kernels: each program
 at 2^21 and 2^24 points under stage depths / block sizes, timed as one graph
 replay after a clean L2 flush and 20 back-to-back launches in one graph.
-Usage: PYTHONPATH=. python scripts/tune_stage.py [grid] > tune_stage.jsonl"""
+Usage: PYTHONPATH=. python scripts/tune_stage.py [grid|frac] > tune_stage.jsonl"""
 
 import json
 import os
@@ -10,13 +10,19 @@ import sys
 
 VARIANTS = {"policy": {}, "nostage": {"TLK_STAGE": "0"},
             "nostage_h0": {"TLK_STAGE": "0", "TLK_HOIST": "0"}}
+if len(sys.argv) > 1 and sys.argv[1] == "frac":
+    VARIANTS = {"policy": {}}
+    for th in (128, 256):
+        for fr in ("0.5", "0.625", "0.75", "0.875", "1.0"):
+            VARIANTS[f"g3x{th}f{fr}"] = {"TLK_STAGE": "3", "TLK_STAGE_THREADS": str(th),
+                                         "TLK_STAGE_FRAC": fr}
 if len(sys.argv) > 1 and sys.argv[1] == "grid":
     for st in (2, 3, 4, 6):
         for th in (128, 256):
             VARIANTS[f"g{st}x{th}"] = {"TLK_STAGE": str(st), "TLK_STAGE_THREADS": str(th)}
 
 CHILD = r"""
-import json, statistics, torch
+import json, statistics, sys, torch
 from paper_1804_10120_b200 import bench as tb, eval_program, capture_graph
 from paper_1804_10120_b200.evaluator import plan_for, kernel_for
 wbuf = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
@@ -39,7 +45,7 @@ def b2b(fn, k=20):
         ts.append(a.elapsed_time(b) / 1e3 / k)
     return statistics.median(ts[1:])
 for name in ("c3_christoffel", "p2", "p3", "c1_dtg", "c2_maxwell"):
-    for n in (1 << 21, 1 << 24, 1 << 26):
+    for n in ((1 << 24, 1 << 26) if len(sys.argv) > 1 and sys.argv[1] == "frac" else (1 << 21, 1 << 24, 1 << 26)):
         prog, vs = tb.load(tb.PROGRAMS[name])
         targets = {v.stmt.lhs.field for v in vs}
         env = tb.make_env(prog, "__none__", 0, tb.DEFAULT_SEED)
@@ -71,7 +77,7 @@ for name in ("c3_christoffel", "p2", "p3", "c1_dtg", "c2_maxwell"):
 
 for vname, knobs in VARIANTS.items():
     env = dict(os.environ, **knobs)
-    res = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True,
+    res = subprocess.run([sys.executable, "-c", CHILD, *sys.argv[1:2]], env=env, capture_output=True, text=True,
                          timeout=900)
     if res.returncode != 0:
         print(json.dumps({"knobs": vname, "error": res.stderr[-800:]}), flush=True)

@@ -286,7 +286,7 @@ def test_fuzzed_programs_match_oracle(seed):
 
 VARIANTS = [dict(restrict=False), dict(hoist=True), dict(vec=1), dict(ldmode=1),
             dict(hoist=True, ldmode=1, vec=1), dict(waves=4), dict(stage=2),
-            dict(stage=3, hoist=True)]
+            dict(stage=3, hoist=True), dict(stage=3, stage_reads=2)]
 
 
 @pytest.mark.parametrize("vkw", VARIANTS, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()))
@@ -460,8 +460,8 @@ def test_size_classes_bitwise_at_the_boundary(name):
 
 
 @pytest.mark.parametrize("name", ["c1_dtg", "c2_maxwell", "c3_christoffel", "p2", "p3"])
-@pytest.mark.parametrize("stage", [2, 4])
-def test_tma_staged_entry_bitwise(name, stage):
+@pytest.mark.parametrize("stage,reads", [(2, 0), (4, 0), (3, 5)])
+def test_tma_staged_entry_bitwise(name, stage, reads):
     # many whole tiles per block (ring wrap-around, mbarrier phase flips), a
     # ragged tail, and an unaligned slab view (falls back to the plain entry)
     from paper_1804_10120_b200 import bench as tb
@@ -475,7 +475,7 @@ def test_tma_staged_entry_bitwise(name, stage):
         env = tb.make_env(prog, targets[0], n, 0xC0FFEE)
         host = {k: f.data.cpu().numpy().copy() for k, f in env.items()}
         _, _, stores = _bind(vs, env)
-        plan = lower_program(vs, variant=Variant(stage=stage))
+        plan = lower_program(vs, variant=Variant(stage=stage, stage_reads=reads))
         if plan.variant.stage == 0:
             pytest.skip("read-modify-write program: no staged entry")
         k = Kernel(plan)
