@@ -487,8 +487,8 @@ class Variant:
           both 1-4 % faster at 2^20;
         * heavier kernels run one point per thread over 4 waves (a launch-
           time choice, same cubin): twice the threads in flight — C3 at
-          128^3 +3 %, P3 +5 %, P2 +4 % at 2^20; the 2-point body wins
-          again from 2^23 points."""
+          64^3 16.4 vs 18.4 us for the staged entry; from 2^21 points the
+          staged entry is ahead (profiles/r01/r01t/tune_smalln.jsonl)."""
         if self.vec == 1 and not self.stage:
             return Variant(**{**self.__dict__, "hoist": True, "small_n": 0})
         return Variant(**{**self.__dict__, "vec": 1, "waves": 4, "small_n": 0})
@@ -525,47 +525,39 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
       twice the blocks in flight hide the per-domain pointer fetch; C4 P2
       5.64 -> 6.10 TB/s, P3 chain 5.10 -> 5.87 TB/s, profiles/r01/tune_batch.jsonl);
     * above the small-N class, read-only-input programs run the TMA-staged
-      entry (tlk_stage_v1: one bulk copy per read slot per tile into a
-      3-deep shared-memory ring) when that ring leaves room for two blocks
-      per SM, or when statements chain (the plain P3 body holds too many
-      registers to keep its loads in flight): C1 +5-7 %, Maxwell +3-4 %,
-      C3 +1-3 %, P3 +3-10 % over the plain entries at 2^24-2^26
-      (profiles/r01/tune_stage*.jsonl).  P2 (40 reads: one block per SM)
-      stays on the plain entry, which holds more bytes in flight.
+      entry (tlk_stage_v1): a 3-deep shared-memory ring fed by one bulk copy
+      per staged read slot per tile, the remaining read slots loaded
+      directly — both in flight together.  Light kernels stage half their
+      reads through 256-point tiles, heavier ones three quarters through
+      128-point tiles (256 when statements chain).  Measured against the
+      plain entries at 2^24-2^26 (profiles/r01/tune_stage_frac.jsonl, back
+      to back): C1 +2-3 %, Maxwell +5-6 %, C3 +6-7 %, P2 +5-7 %, P3 0-3 %;
+      staging every read instead caps P2 (40 reads: one block per SM) below
+      the plain kernel (profiles/r01/bench_stage_ab/).
     """
     arrays = reads + writes
-
-    def ring_tile(tiles) -> int:
-        # largest tile whose 3-deep ring leaves room for two blocks per SM
-        for t in tiles:
-            if 3 * reads * t * 8 <= STAGE_RING_2CTA:
-                return t
-        return 0
-
     if n_ops <= 1.5 * arrays:
-        tile = ring_tile((256, 128)) if rw_slots == 0 else 0
-        return Variant(restrict=True, hoist=tile > 0, ldmode=0, vec=1, waves=4,
-                       small_n=SMALL_N_LIGHT, stage=3 if tile else 0, stage_threads=tile or 128)
+        if rw_slots:
+            return Variant(restrict=True, hoist=False, ldmode=0, vec=1, waves=4,
+                           small_n=SMALL_N_LIGHT)
+        return Variant(restrict=True, hoist=True, ldmode=0, vec=1, waves=4,
+                       small_n=SMALL_N_LIGHT, stage=3, stage_threads=256,
+                       stage_reads=max(1, (reads + 1) // 2))
     if rw_slots == 0:
-        tile = 128 if chained else ring_tile((128,))
         return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=2, waves=4 if chained else 1,
-                       small_n=SMALL_N_HEAVY, stage=3 if tile else 0, stage_threads=tile or 128)
+                       small_n=SMALL_N_HEAVY, stage=3, stage_threads=256 if chained else 128,
+                       stage_reads=max(1, round(0.75 * reads)))
     return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
 
 
 # dynamic shared memory budget of the staged entry's tile ring (bytes; the
 # 227 KB per-block maximum less room for the static mbarriers)
 STAGE_SMEM_MAX = 224 * 1024
-# ring size that still lets two staged blocks share an SM (the policy stages
-# a non-chained program only then: with one block the ring holds too few
-# bytes in flight — P2, 40 reads: 97.9 % vs 99.1 % unstaged at 2^28,
-# profiles/r01/bench_stage_ab/)
-STAGE_RING_2CTA = 112 * 1024
 
 # size classes (Variant.small_class): largest launch, in points, that still
 # runs the small-N choices — the crossovers in profiles/r01/tune_cross.jsonl
 SMALL_N_LIGHT = 1 << 21
-SMALL_N_HEAVY = 1 << 22
+SMALL_N_HEAVY = 1 << 20  # the staged entry already wins at 2^21 (r01t/tune_smalln.jsonl)
 
 
 def _env_variant(v: Variant) -> Variant:

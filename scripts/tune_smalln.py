@@ -21,6 +21,7 @@ VARIANTS_CROSS = {
 }
 VARIANTS = {
     "policy": {},
+    "nosmall": {"TLK_SMALL_N": "0"},  # the large-N choice (staged entry) at every size
     "h1": {"TLK_HOIST": "1"},
     "l1": {"TLK_LDMODE": "1"},
     "h1l1": {"TLK_HOIST": "1", "TLK_LDMODE": "1"},
