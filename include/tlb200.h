@@ -117,7 +117,11 @@ int tlb_batch_create(tlb_kernel* k, int ndom, const void* const* field_bases,
                      const long long* pitches, const long long* ns, void* stream,
                      tlb_batch** out);
 /* vec: 0 = 2-point variant when every slot of every domain is 16-byte
- * aligned, 1 = force the 1-point variant. */
+ * aligned, 1 = force the 1-point variant, 3 = the TMA-staged batch entry
+ * tlk_stage_batch_v1 (modules lowered with a staged variant; otherwise the
+ * 1-point variant; its work-item list is built and uploaded by the first
+ * staged launch, so make that one outside stream capture).  `threads`
+ * applies to the plain entries only. */
 int tlb_batch_launch(tlb_batch* b, int vec, int threads, void* stream);
 void tlb_batch_destroy(tlb_batch* b);
 

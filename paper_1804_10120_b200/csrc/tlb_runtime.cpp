@@ -235,11 +235,11 @@ int ctx_state(CUcontext ctx, CtxState** out) {
 
 // ---------------------------------------------------------------- kernel ----
 
-// STAGE_V1 (the TMA-staged entry) exists only in modules lowered with a
-// staged variant; the others are in every module
-enum Entry { FLAT_V1 = 0, FLAT_V2, BATCH_V1, BATCH_V2, STAGE_V1, N_ENTRIES };
-const char* kEntryNames[N_ENTRIES] = {"tlk_flat_v1", "tlk_flat_v2", "tlk_batch_v1",
-                                      "tlk_batch_v2", "tlk_stage_v1"};
+// STAGE_V1 / STAGE_BATCH_V1 (the TMA-staged entries) exist only in modules
+// lowered with a staged variant; the others are in every module
+enum Entry { FLAT_V1 = 0, FLAT_V2, BATCH_V1, BATCH_V2, STAGE_V1, STAGE_BATCH_V1, N_ENTRIES };
+const char* kEntryNames[N_ENTRIES] = {"tlk_flat_v1",  "tlk_flat_v2",  "tlk_batch_v1",
+                                      "tlk_batch_v2", "tlk_stage_v1", "tlk_stage_batch_v1"};
 
 struct Loaded {
   CUmodule mod = nullptr;
@@ -259,6 +259,7 @@ struct tlb_kernel {
   int threads = 256;   // compiled TLK_THREADS: default block size (from the source)
   int stage_threads = 0;  // block size (= tile) of tlk_stage_v1 (from the source)
   int stage_smem = 0;     // its dynamic shared memory (from the source)
+  int stage_batch_smem = 0;  // tlk_stage_batch_v1's: the ring + NSTAGE x NSLOTS pointers
   std::mutex mu;
   std::map<CUcontext, Loaded> loaded;
 };
@@ -267,6 +268,9 @@ struct tlb_batch {
   tlb_kernel* k = nullptr;
   CUcontext ctx = nullptr;
   CUdeviceptr table = 0;
+  CUdeviceptr items = 0;  // staged batch: {domain | count << 32, first point} per tile
+  long long nitems = -1;  // -1: not built yet (first staged launch builds them)
+  std::vector<long long> ns;
   int ndom = 0;
   long long max_n = 0;
   bool vec2 = false;
@@ -284,21 +288,21 @@ int load_module(tlb_kernel* k, CUcontext ctx, Loaded** out) {
   Loaded L;
   CU(g_cu.ModuleLoadData(&L.mod, k->cubin.data()), "cuModuleLoadData");
   for (int e = 0; e < N_ENTRIES; ++e) {
-    if (e == STAGE_V1) {
-      if (k->stage_smem <= 0 ||
+    int block = k->threads, smem = 0;
+    if (e == STAGE_V1 || e == STAGE_BATCH_V1) {
+      smem = e == STAGE_V1 ? k->stage_smem : k->stage_batch_smem;
+      block = k->stage_threads + (e == STAGE_BATCH_V1 ? 32 : 0);
+      if (smem <= 0 ||
           g_cu.ModuleGetFunction(&L.fn[e], L.mod, kEntryNames[e]) != CUDA_SUCCESS) {
         L.fn[e] = nullptr;
         continue;
       }
-      CU(g_cu.FuncSetAttribute(L.fn[e], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                               k->stage_smem),
+      CU(g_cu.FuncSetAttribute(L.fn[e], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem),
          "cuFuncSetAttribute(stage smem)");
     } else {
       CU(g_cu.ModuleGetFunction(&L.fn[e], L.mod, kEntryNames[e]), kEntryNames[e]);
     }
-    CU(g_cu.OccupancyMaxActiveBlocksPerMultiprocessor(
-           &L.occ[e], L.fn[e], e == STAGE_V1 ? k->stage_threads : k->threads,
-           e == STAGE_V1 ? k->stage_smem : 0),
+    CU(g_cu.OccupancyMaxActiveBlocksPerMultiprocessor(&L.occ[e], L.fn[e], block, smem),
        "cuOccupancyMaxActiveBlocksPerMultiprocessor");
     if (L.occ[e] < 1) L.occ[e] = 1;
   }
@@ -405,6 +409,8 @@ int tlb_compile(const char* src, const char* const* opts, int nopts, const char*
         nstage * source_define(src, "TLK_NREAD", 1) * k->stage_threads * 8;
     if (smem > 227 * 1024) return fail("tlb_compile: staged tile ring of %lld bytes", smem);
     k->stage_smem = (int)smem;
+    const long long bsmem = smem + nstage * source_define(src, "TLK_NSLOTS", 0) * 8;
+    k->stage_batch_smem = bsmem <= 227 * 1024 ? (int)bsmem : 0;  // 0: no staged batch
   }
   if (file_exists(cache_path) && read_file(cache_path, &k->cubin)) {
     *out = k.release();
@@ -594,6 +600,7 @@ int tlb_batch_create(tlb_kernel* k, int ndom, const void* const* field_bases,
   CU(g_cu.MemAlloc(&b->table, table.size() * sizeof(uint64_t)), "cuMemAlloc(batch table)");
   CU(g_cu.MemcpyHtoD(b->table, table.data(), table.size() * sizeof(uint64_t)),
      "cuMemcpyHtoD(batch table)");
+  if (k->stage_batch_smem > 0) b->ns.assign(ns, ns + ndom);  // staged items: built on demand
   *out = b.release();
   return 0;
 }
@@ -608,6 +615,38 @@ int tlb_batch_launch(tlb_batch* b, int vec, int threads, void* stream) {
   if (ctx_state(ctx, &st)) return 1;
   Loaded* L;
   if (load_module(b->k, ctx, &L)) return 1;
+  if (vec == 3 && L->fn[STAGE_BATCH_V1] && b->nitems < 0) {
+    // work items of the staged batch entry: every (domain, tile) pair
+    const long long tile = b->k->stage_threads;
+    std::vector<long long> items;
+    for (size_t d = 0; d < b->ns.size(); ++d)
+      for (long long x = 0; x < b->ns[d]; x += tile) {
+        const long long cnt = std::min(tile, b->ns[d] - x);
+        items.push_back((long long)d | (cnt << 32));
+        items.push_back(x);
+      }
+    if (!items.empty()) {
+      CU(g_cu.MemAlloc(&b->items, items.size() * sizeof(long long)), "cuMemAlloc(batch items)");
+      CU(g_cu.MemcpyHtoD(b->items, items.data(), items.size() * sizeof(long long)),
+         "cuMemcpyHtoD(batch items)");
+    }
+    b->nitems = (long long)items.size() / 2;
+  }
+  if (vec == 3 && b->nitems == 0) return 0;  // only empty domains
+  if (vec == 3 && b->items && L->fn[STAGE_BATCH_V1]) {
+    // staged batch: persistent blocks of stage_threads consumers + a producer warp
+    long long blocks =
+        std::min<long long>(b->nitems, (long long)st->sm_count * L->occ[STAGE_BATCH_V1]);
+    CUdeviceptr table = b->table, items = b->items;
+    long long nitems = b->nitems;
+    void* args[] = {&table, &items, &nitems};
+    CU(g_cu.LaunchKernel(L->fn[STAGE_BATCH_V1], (unsigned)std::max(1LL, blocks), 1, 1,
+                         (unsigned)(b->k->stage_threads + 32), 1, 1,
+                         (unsigned)b->k->stage_batch_smem, (CUstream)stream, args, nullptr),
+       "cuLaunchKernel(stage batch)");
+    return 0;
+  }
+  if (vec == 3) vec = 1;  // no staged batch entry: the 1-point batch entry
   const bool v2 = b->vec2 && vec != 1;
   const int e = v2 ? BATCH_V2 : BATCH_V1;
   if (threads <= 0) threads = b->k->threads;
@@ -641,6 +680,7 @@ void tlb_batch_destroy(tlb_batch* b) {
     g_cu.CtxGetCurrent(&cur);
     if (cur != b->ctx) g_cu.CtxSetCurrent(b->ctx);
     g_cu.MemFree(b->table);
+    if (b->items) g_cu.MemFree(b->items);
     if (cur && cur != b->ctx) g_cu.CtxSetCurrent(cur);
   }
   delete b;

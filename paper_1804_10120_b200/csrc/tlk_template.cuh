@@ -299,4 +299,102 @@ tlk_stage_v1(const tlk_flat_params prm) {
        x += stride)
     tlk_point<double>(prm, x);
 }
+
+// tlk_stage_batch_v1: the multi-domain batch through the same ring, with a
+// dedicated producer warp (block = TLK_STAGE_THREADS consumers + 32).  Work
+// items are (domain, tile) pairs, built on the host at tlb_batch_create:
+// items[w] = {domain | count << 32, first point}.  Per item the producer warp
+// reads the domain's slot pointers from the batch table into the stage's
+// pointer block (lanes stride over slots), then lane 0 issues the bulk
+// copies of the staged read slots (full[s] completes on their bytes plus 32
+// lane arrivals).  Tiles with an odd count or any slot not 16-byte aligned
+// are not copied: their count is stored negated and consumers read every
+// slot from global memory.  Consumers release a stage through empty[s]; the
+// producer refills it NSTAGE items later.  Pointer block: NSTAGE x NSLOTS
+// pointers after the ring.
+__device__ __forceinline__ void tlk_mbar_wait(unsigned b, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TLK_BWAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TLK_BWAIT_%=;\n}" ::"r"(b), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tlk_mbar_arrive(unsigned b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+}
+
+extern "C" __global__ void __launch_bounds__(TLK_STAGE_THREADS + 32)
+tlk_stage_batch_v1(const long long* __restrict__ table, const longlong2* __restrict__ items,
+                   long long nitems) {
+  constexpr int kRord[TLK_NSLOTS] = TLK_RORD;
+  constexpr int kTile = TLK_STAGE_THREADS;
+  extern __shared__ __align__(128) double tlk_sm[];
+  double** ptrs = reinterpret_cast<double**>(tlk_sm + (long long)TLK_NSTAGE * TLK_NREAD * kTile);
+  __shared__ int cnts[TLK_NSTAGE];
+  __shared__ __align__(8) unsigned long long full[TLK_NSTAGE], empty[TLK_NSTAGE];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < TLK_NSTAGE; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(tlk_smem_addr(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tlk_smem_addr(&empty[s])),
+                   "r"(kTile));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid >= kTile) {  // producer warp
+    const int lane = tid - kTile;
+    int k = 0;
+    for (long long w = blockIdx.x; w < nitems; w += gridDim.x, ++k) {
+      const int s = k % TLK_NSTAGE;
+      if (k >= TLK_NSTAGE)
+        tlk_mbar_wait(tlk_smem_addr(&empty[s]), (unsigned)(k / TLK_NSTAGE - 1) & 1u);
+      const longlong2 item = items[w];
+      const long long d = item.x & 0xffffffffLL;
+      const int cnt = (int)(item.x >> 32);
+      const long long* rec = table + d * (TLK_NSLOTS + 1);
+      bool ok = (cnt & 1) == 0;
+      for (int j = lane; j < TLK_NSLOTS; j += 32) {
+        double* g = reinterpret_cast<double*>(__ldg(rec + 1 + j)) + item.y;
+        ok = ok && (reinterpret_cast<unsigned long long>(g) & 15ull) == 0;
+        ptrs[s * TLK_NSLOTS + j] = g;
+      }
+      ok = __all_sync(0xffffffffu, ok);
+      if (lane == 0) cnts[s] = ok ? cnt : -cnt;
+      __syncwarp();
+      const unsigned fb = tlk_smem_addr(&full[s]);
+      if (ok && lane == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(fb), "r"((unsigned)(TLK_NREAD * cnt * sizeof(double))) : "memory");
+#pragma unroll
+        for (int j = 0; j < TLK_NSLOTS; ++j) {
+          if (kRord[j] < 0) continue;
+          double* dst = tlk_sm + ((long long)s * TLK_NREAD + kRord[j]) * kTile;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+              "[%3];" ::"r"(tlk_smem_addr(dst)), "l"(ptrs[s * TLK_NSLOTS + j]),
+              "r"((unsigned)(cnt * sizeof(double))), "r"(fb) : "memory");
+        }
+      } else {
+        tlk_mbar_arrive(fb);
+      }
+    }
+  } else {  // consumers
+    int k = 0;
+    for (long long w = blockIdx.x; w < nitems; w += gridDim.x, ++k) {
+      const int s = k % TLK_NSTAGE;
+      tlk_mbar_wait(tlk_smem_addr(&full[s]), (unsigned)(k / TLK_NSTAGE) & 1u);
+      const int c = cnts[s];
+      tlk_flat_params q;
+      q.n = 0;
+#pragma unroll
+      for (int j = 0; j < TLK_NSLOTS; ++j)
+        q.p[j] = (c > 0 && kRord[j] >= 0)
+                     ? tlk_sm + ((long long)s * TLK_NREAD + kRord[j]) * kTile
+                     : ptrs[s * TLK_NSLOTS + j];
+      if (tid < (c < 0 ? -c : c)) tlk_point<double, 3>(q, tid);
+      tlk_mbar_arrive(tlk_smem_addr(&empty[s]));
+    }
+  }
+}
 #endif

@@ -460,7 +460,7 @@ class Variant:
     ldmode: int = 0
     vec: int = 2
     waves: int = 1
-    batch_vec: int = 1  # points per thread of the multi-domain batch entry
+    batch_vec: int = 1  # batch entry: points per thread (1, 2), or 3 = the staged batch entry
     batch_ptrs: int = 0  # TLK_BATCH_PTRS: 0 shared-memory staging, 1 direct table reads
     small_n: int = 0  # launches of <= small_n points run small_class() (0: never)
     stage: int = 0  # >0: TMA-staged entry tlk_stage_v1 with a `stage`-deep tile ring

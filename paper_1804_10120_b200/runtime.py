@@ -170,7 +170,10 @@ class Kernel:
             self.vec = 3  # the staged entry (its tile ring size is read from the source)
         if var is not None and var.waves > 1 and self.max_blocks == 0:
             self.max_blocks = -var.waves
+        # batch entry: 0 = 2-point when aligned, 1 = 1-point, 3 = TMA-staged
         self.batch_vec = 1 if (var is not None and var.batch_vec == 1) else 0
+        if var is not None and var.batch_vec == 3:
+            self.batch_vec = 3 if var.stage else 1
         # size class (Variant.small_class): launches of <= small_n points run
         # `small` (a second cubin when the code differs, else this one) with
         # its own vec/waves; set by get_kernel

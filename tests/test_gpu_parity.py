@@ -488,3 +488,41 @@ def test_tma_staged_entry_bitwise(name, stage, reads):
         for t in targets:
             got = env[t].data.cpu().numpy()[..., lo:]
             assert same_bits(got, sub[t]), (n, lo, t)
+
+
+@pytest.mark.parametrize("tile,reads", [(128, 0), (256, 0), (128, 7)])
+@pytest.mark.parametrize("name", ["c4_p2", "c4_p3"])
+def test_tma_staged_batch_entry_bitwise(name, tile, reads):
+    # the warp-specialised staged batch: ragged domains (odd counts and odd
+    # pitches take the uncopied path), several items per block, ring reuse
+    from paper_1804_10120_b200.evaluator import _bind
+    from paper_1804_10120_b200.lowering import Variant, lower_program
+    from paper_1804_10120_b200.runtime import Batch, Kernel
+
+    prog, vs = program(manifest()["cases"][name]["source"])
+    targets = sorted({v.stmt.lhs.field for v in vs})
+    sizes = [1, 2, 3, 100, 4097, 4096, 255, 20000, 6] + [4096] * 300
+    envs, hosts = [], []
+    for d, n in enumerate(sizes):
+        host = random_host_env(prog, n, 70 + d)
+        for t in targets:
+            host[t][:] = 0.0
+        hosts.append(host)
+        envs.append(device_env(prog, host))
+    plan = lower_program(vs, variant=Variant(stage=3, stage_threads=tile, stage_reads=reads,
+                                             batch_vec=3))
+    kern = Kernel(plan)
+    assert kern.batch_vec == 3
+    bases, pitches = [], []
+    for env in envs:
+        _, _, stores = _bind(vs, env)
+        bases.append([s.base for s in stores])
+        pitches.append([s.pitch for s in stores])
+    stream = torch.cuda.current_stream().cuda_stream
+    Batch(kern, bases, pitches, sizes, stream).launch(stream)
+    torch.cuda.synchronize()
+    for env, host in zip(envs, hosts):
+        numpy_eval.eval_program(vs, host)
+        got = env_to_host(env)
+        for t in targets:
+            assert same_bits(got[t], host[t]), (t, host[t].shape)
