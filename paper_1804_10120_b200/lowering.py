@@ -536,8 +536,11 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
       the plain kernel (profiles/r01/bench_stage_ab/).
     """
     arrays = reads + writes
+    # the staged entries unroll per-slot loops: beyond a few hundred slots
+    # (unmeasured territory, slow NVRTC compiles) the plain entries are used
+    stageable = rw_slots == 0 and arrays <= STAGE_MAX_SLOTS
     if n_ops <= 1.5 * arrays:
-        if rw_slots:
+        if not stageable:
             return Variant(restrict=True, hoist=False, ldmode=0, vec=1, waves=4,
                            small_n=SMALL_N_LIGHT)
         return Variant(restrict=True, hoist=True, ldmode=0, vec=1, waves=4,
@@ -545,7 +548,8 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
                        stage_reads=max(1, (reads + 1) // 2))
     if rw_slots == 0:
         return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=2, waves=4 if chained else 1,
-                       small_n=SMALL_N_HEAVY, stage=3, stage_threads=256 if chained else 128,
+                       small_n=SMALL_N_HEAVY, stage=3 if stageable else 0,
+                       stage_threads=256 if chained else 128,
                        stage_reads=max(1, round(0.75 * reads)))
     return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
 
@@ -553,6 +557,9 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
 # dynamic shared memory budget of the staged entry's tile ring (bytes; the
 # 227 KB per-block maximum less room for the static mbarriers)
 STAGE_SMEM_MAX = 224 * 1024
+
+# largest program (read + written component arrays) the policy stages
+STAGE_MAX_SLOTS = 256
 
 # size classes (Variant.small_class): largest launch, in points, that still
 # runs the small-N choices — the crossovers in profiles/r01/tune_cross.jsonl
