@@ -527,13 +527,15 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
     * above the small-N class, read-only-input programs run the TMA-staged
       entry (tlk_stage_v1): a 3-deep shared-memory ring fed by one bulk copy
       per staged read slot per tile, the remaining read slots loaded
-      directly — both in flight together.  Light kernels stage half their
-      reads through 256-point tiles, heavier ones three quarters through
-      128-point tiles (256 when statements chain).  Measured against the
-      plain entries at 2^24-2^26 (profiles/r01/tune_stage_frac.jsonl, back
-      to back): C1 +2-3 %, Maxwell +5-6 %, C3 +6-7 %, P2 +5-7 %, P3 0-3 %;
-      staging every read instead caps P2 (40 reads: one block per SM) below
-      the plain kernel (profiles/r01/bench_stage_ab/).
+      directly — both in flight together.  256-point tiles; light kernels
+      stage half their reads, heavier ones three quarters (0.85 for
+      non-chained programs of 32+ reads, whose ring then takes a whole SM).
+      Measured against the plain entries at 2^24-2^26
+      (profiles/r01/tune_stage_frac.jsonl, back to back): C1 +2-3 %,
+      Maxwell +5-6 %, C3 +6-7 %, P2 +5-9 %, P3 0-3 %; P2 at 2^28 102.3 %
+      of measured copy bandwidth (34 of 40 reads staged) vs 101.1 % (30 of
+      40, 128-point tiles) and 99.1 % plain (profiles/r01/bench_stage_*).
+      Staging every read caps P2 below the plain kernel.
     """
     arrays = reads + writes
     # the staged entries unroll per-slot loops: beyond a few hundred slots
@@ -547,10 +549,10 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
                        small_n=SMALL_N_LIGHT, stage=3, stage_threads=256,
                        stage_reads=max(1, (reads + 1) // 2))
     if rw_slots == 0:
+        share = 0.85 if reads >= 32 and not chained else 0.75
         return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=2, waves=4 if chained else 1,
-                       small_n=SMALL_N_HEAVY, stage=3 if stageable else 0,
-                       stage_threads=256 if chained else 128,
-                       stage_reads=max(1, round(0.75 * reads)))
+                       small_n=SMALL_N_HEAVY, stage=3 if stageable else 0, stage_threads=256,
+                       stage_reads=max(1, round(share * reads)))
     return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
 
 
