@@ -462,6 +462,7 @@ class Variant:
     waves: int = 1
     batch_vec: int = 1  # batch entry: points per thread (1, 2), or 3 = the staged batch entry
     batch_ptrs: int = 0  # TLK_BATCH_PTRS: 0 shared-memory staging, 1 direct table reads
+    batch_threads: int = 0  # block size of the plain batch entries (0 = threads)
     small_n: int = 0  # launches of <= small_n points run small_class() (0: never)
     stage: int = 0  # >0: TMA-staged entry tlk_stage_v1 with a `stage`-deep tile ring
     threads: int = 256  # TLK_THREADS: block size of the flat and batch entries
@@ -472,6 +473,7 @@ class Variant:
         t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
              f"v{self.vec}w{self.waves}b{self.batch_vec}{self.batch_ptrs}")
         t += f"s{self.small_n.bit_length() - 1}" if self.small_n else ""
+        t += f"k{self.batch_threads}" if self.batch_threads else ""
         t += f"g{self.stage}x{self.stage_threads}" if self.stage else ""
         t += f"r{self.stage_reads}" if self.stage and self.stage_reads else ""
         return t + (f"n{self.threads}" if self.threads != 256 else "")
@@ -587,6 +589,8 @@ def _env_variant(v: Variant) -> Variant:
         kw["batch_vec"] = int(env["TLK_BATCH_VEC"])
     if "TLK_BATCH_PTRS" in env:
         kw["batch_ptrs"] = int(env["TLK_BATCH_PTRS"])
+    if "TLK_BATCH_THREADS" in env:
+        kw["batch_threads"] = int(env["TLK_BATCH_THREADS"])
     if "TLK_STAGE" in env:
         kw["stage"] = int(env["TLK_STAGE"])
     if "TLK_THREADS" in env:

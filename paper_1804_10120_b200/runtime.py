@@ -174,6 +174,8 @@ class Kernel:
         self.batch_vec = 1 if (var is not None and var.batch_vec == 1) else 0
         if var is not None and var.batch_vec == 3:
             self.batch_vec = 3 if var.stage else 1
+        self.batch_threads = (var.batch_threads if var is not None and var.batch_threads
+                              else self.threads)
         # size class (Variant.small_class): launches of <= small_n points run
         # `small` (a second cubin when the code differs, else this one) with
         # its own vec/waves; set by get_kernel
@@ -259,7 +261,7 @@ class Batch:
         self.ndom = len(ns)
 
     def launch(self, stream: int, threads: int | None = None) -> None:
-        threads = self.kernel.threads if threads is None else threads
+        threads = self.kernel.batch_threads if threads is None else threads
         check(lib().tlb_batch_launch(self.handle, self.kernel.batch_vec, threads, stream),
               "tlb_batch_launch")
         self.kernel.launches += 1

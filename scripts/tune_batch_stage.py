@@ -1,7 +1,7 @@
 """C4 (512 subdomains of 16^3 points, one launch) through the plain batch
 entry and the TMA-staged batch entry under ring shapes: one graph replay
 after a clean L2 flush, and 20 back-to-back launches in one graph.
-Usage: PYTHONPATH=. python scripts/tune_batch_stage.py > tune_batch_stage.jsonl"""
+Usage: PYTHONPATH=. python scripts/tune_batch_stage.py [threads] > out.jsonl"""
 
 import json
 import os
@@ -9,10 +9,18 @@ import subprocess
 import sys
 
 VARIANTS = {"policy": {}, "staged": {"TLK_BATCH_VEC": "3"}}
-for th in (128, 256):
-    for fr in ("0.5", "0.75", "1.0"):
-        VARIANTS[f"staged_x{th}f{fr}"] = {"TLK_BATCH_VEC": "3", "TLK_STAGE_THREADS": str(th),
-                                          "TLK_STAGE_FRAC": fr}
+if len(sys.argv) > 1 and sys.argv[1] == "threads":
+    VARIANTS = {"policy": {}}
+    for th in (64, 128, 192):
+        VARIANTS[f"bt{th}"] = {"TLK_BATCH_THREADS": str(th)}
+        VARIANTS[f"bt{th}_v2"] = {"TLK_BATCH_THREADS": str(th), "TLK_BATCH_VEC": "2"}
+    VARIANTS["bptrs1_bt128"] = {"TLK_BATCH_THREADS": "128", "TLK_BATCH_PTRS": "1"}
+else:
+    for th in (128, 256):
+        for fr in ("0.5", "0.75", "1.0"):
+            VARIANTS[f"staged_x{th}f{fr}"] = {"TLK_BATCH_VEC": "3",
+                                              "TLK_STAGE_THREADS": str(th),
+                                              "TLK_STAGE_FRAC": fr}
 
 CHILD = r"""
 import json, statistics, torch
