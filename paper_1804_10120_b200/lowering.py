@@ -525,7 +525,9 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
     * the multi-domain batch entry always runs one point per thread with the
       domain's slot pointers staged in shared memory (small 16^3 domains:
       twice the blocks in flight hide the per-domain pointer fetch; C4 P2
-      5.64 -> 6.10 TB/s, P3 chain 5.10 -> 5.87 TB/s, profiles/r01/tune_batch.jsonl);
+      5.64 -> 6.10 TB/s, P3 chain 5.10 -> 5.87 TB/s, profiles/r01/tune_batch.jsonl),
+      in 128-thread blocks for the heavier kernels (C4 P2 163.8 -> 159.7 us,
+      P3 200.7 -> 196.6 us, profiles/r01/tune_batch_threads.jsonl);
     * above the small-N class, read-only-input programs run the TMA-staged
       entry (tlk_stage_v1): a 3-deep shared-memory ring fed by one bulk copy
       per staged read slot per tile, the remaining read slots loaded
@@ -554,7 +556,7 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
         share = 0.85 if reads >= 32 and not chained else 0.75
         return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=2, waves=4 if chained else 1,
                        small_n=SMALL_N_HEAVY, stage=3 if stageable else 0, stage_threads=256,
-                       stage_reads=max(1, round(share * reads)))
+                       stage_reads=max(1, round(share * reads)), batch_threads=128)
     return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
 
 
