@@ -271,6 +271,10 @@ def run_ours(args, dist: Dist) -> dict | None:
     ms_per_step = total_ms / args.steps
     value = args.points / (ms_per_step / 1e3)
     peak, peak_src = measured_peak()
+    from paper_1804_10120_b200.runtime import fp64_peak_gflops
+
+    fp64_peak = fp64_peak_gflops()
+    flops = plan.flops_per_point * n_local  # per launch, this rank
     alg_bytes = plan.bytes_per_point * n_local  # per launch, this rank
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9  # this rank's kernel (rank 0 reports)
     traffic = None
@@ -340,6 +344,14 @@ def run_ours(args, dist: Dist) -> dict | None:
             "kernel_ms": kernel_ms,
             "kernel_ms_max_over_ranks": kernel_ms_max,
             "algorithmic_bytes_per_launch": alg_bytes,
+            # the flop side: the slower of bytes/HBM and flops/FP64 binds
+            "fp64_peak_gflops": fp64_peak,
+            "fp64_peak_source": "measured: tlb_fp64_probe (uncontracted DMUL+DADD, the fused "
+                                "kernels' instruction mix)",
+            "fp64_achieved_gflops": flops / (kernel_ms / 1e3) / 1e9,
+            "fp64_frac": flops / (kernel_ms / 1e3) / 1e9 / fp64_peak,
+            "hbm_bound_ms": alg_bytes / (peak * 1e9) * 1e3,
+            "fp64_bound_ms": flops / (fp64_peak * 1e9) * 1e3,
         },
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -516,6 +528,9 @@ def run_configs() -> dict:
     from paper_1804_10120_b200.evaluator import plan_for
 
     peak, _ = measured_peak()
+    from paper_1804_10120_b200.runtime import fp64_peak_gflops
+
+    fp64_peak = fp64_peak_gflops()
     flush = L2Flush()
 
     def timed(fn):
@@ -550,6 +565,9 @@ def run_configs() -> dict:
                     "hbm_gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
                     "us_b2b": round(t_b2b * 1e6, 2),
                     "frac_b2b": round(plan.bytes_per_point * n / t_b2b / 1e9 / peak, 4),
+                    "fp64_frac": round(plan.flops_per_point * n / t / 1e9 / fp64_peak, 4),
+                    "bound": ("hbm" if plan.bytes_per_point / peak
+                              >= plan.flops_per_point / fp64_peak else "fp64"),
                     "variant": plan.variant.tag() if plan.variant else None}
 
     for key, text, n in (("C1_dtg_64^3", tb.DTG, 64**3),
@@ -595,11 +613,14 @@ def run_configs() -> dict:
     del envs3
     tiny = torch.zeros(1, device="cuda")
     out["floor_us"] = round(timed(lambda: tiny.add_(1.0))[0] * 1e6, 2)
+    out["fp64_peak_gflops"] = round(fp64_peak, 1)
     out["method"] = ("us/frac: one CUDA-graph replay bracketed by events after an L2 flush "
                      "(256 MB write, then 256 MB read: L2 cold and clean, so no write-back of "
                      "the flush's dirty lines is billed to the kernel), median of 11; "
                      "floor_us: the same measurement of a graph holding one 1-element kernel "
-                     "(graph launch + event overhead); us_b2b/frac_b2b: steady state, 20 "
+                     "(graph launch + event overhead); fp64_frac: flops / time / the measured "
+                     "uncontracted fp64 peak (fp64_peak_gflops), bound: the side of the "
+                     "roofline that binds; us_b2b/frac_b2b: steady state, 20 "
                      "back-to-back launches in one graph (inputs re-read from L2 when the "
                      "working set fits); hbm_gbs/frac use the fused program's algorithmic "
                      "bytes (for *_arrays_mode that is the paper's BW_eff, not the traffic)")

@@ -174,6 +174,14 @@ int tlb_harness_call(tlb_harness_kernel* hk, long n, double** const* tensors,
 int tlb_fill_uniform(double* dst, long long n, unsigned long long seed,
                      unsigned long long stream_id, long long offset, void* stream);
 
+/* FP64 throughput probe (the flop side of the roofline): `blocks` blocks of
+ * 256 threads, each thread running 8 independent chains of `iters` uncontracted
+ * DMUL+DADD steps (2 flops each) — the instruction mix of the fused kernels,
+ * which are compiled without FMA contraction.  `out` (one double) is written
+ * only to keep the chains live.  Asynchronous on `stream`; time it with
+ * events: flops = blocks * 256 * iters * 16. */
+int tlb_fp64_probe(double* out, int blocks, int iters, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

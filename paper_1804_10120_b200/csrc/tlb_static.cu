@@ -35,9 +35,39 @@ __global__ void __launch_bounds__(256) fill_uniform_kernel(double* __restrict__ 
   }
 }
 
+// FP64 throughput probe for the flop side of the roofline.  The fused
+// kernels are compiled without FMA contraction (bit-exact parity), so their
+// flops are separate DMUL/DADD instructions: the probe times exactly that
+// mix — 8 independent mul+add chains per thread (__dmul_rn/__dadd_rn are
+// never contracted), 2 flops per chain step.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* __restrict__ out, int iters) {
+  double a[8], m = 1.0 + 1e-12 * threadIdx.x, c = 1e-9;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0 + k * 1e-3 + blockIdx.x * 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __dadd_rn(__dmul_rn(a[k], m), c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 0.123456789) out[0] = s;  // keeps the chains live; never true in practice
+}
+
 }  // namespace
 
 void tlb_internal_set_error(const char* msg);  // tlb_runtime.cpp
+
+extern "C" int tlb_fp64_probe(double* out, int blocks, int iters, void* stream) {
+  if (blocks < 1 || iters < 1) return 0;
+  fp64_probe_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(out, iters);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    tlb_internal_set_error(cudaGetErrorString(e));
+    return 1;
+  }
+  return 0;
+}
 
 extern "C" int tlb_fill_uniform(double* dst, long long n, unsigned long long seed,
                                 unsigned long long stream_id, long long offset, void* stream) {

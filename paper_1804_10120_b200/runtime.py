@@ -36,6 +36,7 @@ EXPORTED = (
     "tlb_kernel_set_slots", "tlb_kernel_attrs", "tlb_launch",
     "tlb_batch_create",
     "tlb_batch_launch", "tlb_batch_destroy", "tlb_exec_host", "tlb_fill_uniform",
+    "tlb_fp64_probe",
     "tlb_harness_call", "tlb_release_staging",
 )
 
@@ -91,6 +92,7 @@ def lib() -> ctypes.CDLL:
                 "tlb_fill_uniform": (c_int, [c_vp, c_ll, ctypes.c_ulonglong, ctypes.c_ulonglong,
                                              c_ll, c_vp]),
                 "tlb_release_staging": (c_int, []),
+                "tlb_fp64_probe": (c_int, [c_vp, c_int, c_int, c_vp]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -315,3 +317,24 @@ def fill_uniform(t, seed: int, stream_id: int, offset: int = 0, stream: int | No
     with torch.cuda.device(t.device):
         check(lib().tlb_fill_uniform(t.data_ptr(), t.numel(), seed, stream_id, offset, stream),
               "tlb_fill_uniform")
+
+
+def fp64_peak_gflops(iters: int = 4096, reps: int = 5) -> float:
+    """Measured uncontracted fp64 throughput (DMUL + DADD, GFLOP/s) of the
+    current device: the flop side of the roofline (tlb_fp64_probe)."""
+    import torch
+
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    sms = torch.cuda.get_device_properties(out.device).multi_processor_count
+    blocks = sms * 8
+    stream = torch.cuda.current_stream().cuda_stream
+    check(lib().tlb_fp64_probe(out.data_ptr(), blocks, 64, stream), "tlb_fp64_probe")
+    best = float("inf")
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        check(lib().tlb_fp64_probe(out.data_ptr(), blocks, iters, stream), "tlb_fp64_probe")
+        b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b) / 1e3)
+    return blocks * 256 * iters * 16 / best / 1e9

@@ -1,7 +1,7 @@
 """TMA-staged entry (tlk_stage_v1) against the policy kernels: each program
 at 2^21 and 2^24 points under stage depths / block sizes, timed as one graph
 replay after a clean L2 flush and 20 back-to-back launches in one graph.
-Usage: PYTHONPATH=. python scripts/tune_stage.py [grid|frac] > tune_stage.jsonl"""
+Usage: PYTHONPATH=. python scripts/tune_stage.py [grid|frac|light] > tune_stage.jsonl"""
 
 import json
 import os
@@ -16,6 +16,12 @@ if len(sys.argv) > 1 and sys.argv[1] == "frac":
         for fr in ("0.5", "0.625", "0.75", "0.875", "1.0"):
             VARIANTS[f"g3x{th}f{fr}"] = {"TLK_STAGE": "3", "TLK_STAGE_THREADS": str(th),
                                          "TLK_STAGE_FRAC": fr}
+if len(sys.argv) > 1 and sys.argv[1] == "light":
+    VARIANTS = {"policy": {}}
+    for depth in (3, 4):
+        for r in (4, 6, 8, 10, 12, 14, 16):
+            VARIANTS[f"g{depth}x256r{r}"] = {"TLK_STAGE": str(depth), "TLK_STAGE_THREADS": "256",
+                                            "TLK_STAGE_READS": str(r)}
 if len(sys.argv) > 1 and sys.argv[1] == "grid":
     for st in (2, 3, 4, 6):
         for th in (128, 256):
@@ -44,8 +50,10 @@ def b2b(fn, k=20):
         a.record(); g.replay(); b.record(); b.synchronize()
         ts.append(a.elapsed_time(b) / 1e3 / k)
     return statistics.median(ts[1:])
-for name in ("c3_christoffel", "p2", "p3", "c1_dtg", "c2_maxwell"):
-    for n in ((1 << 24, 1 << 26) if len(sys.argv) > 1 and sys.argv[1] == "frac" else (1 << 21, 1 << 24, 1 << 26)):
+for name in (("c1_dtg", "c2_maxwell") if len(sys.argv) > 1 and sys.argv[1] == "light"
+             else ("c3_christoffel", "p2", "p3", "c1_dtg", "c2_maxwell")):
+    for n in ((1 << 24, 1 << 26) if len(sys.argv) > 1 and sys.argv[1] in ("frac", "light")
+              else (1 << 21, 1 << 24, 1 << 26)):
         prog, vs = tb.load(tb.PROGRAMS[name])
         targets = {v.stmt.lhs.field for v in vs}
         env = tb.make_env(prog, "__none__", 0, tb.DEFAULT_SEED)
