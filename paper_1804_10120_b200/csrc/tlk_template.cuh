@@ -233,6 +233,9 @@ tlk_batch_v2(const long long* __restrict__ table, int ndom) {
 // TLK_STAGE_THREADS and the per-slot read ordinals TLK_RORD); needs every
 // read slot 16-byte aligned (the runtime checks).
 #ifdef TLK_NSTAGE
+#if TLK_NREAD < 1
+#error "a staged kernel needs at least one staged read slot (its mbarrier would never complete)"
+#endif
 __device__ __forceinline__ unsigned tlk_smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }

@@ -651,8 +651,9 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         variant = Variant(**{**variant.__dict__, "hoist": hoist_loads})
     if variant.ldmode == 1 and rw:
         variant = Variant(**{**variant.__dict__, "ldmode": 0})  # see Variant docstring
-    if variant.stage and rw:
-        # a staged read-modify-write slot would be stored into its own tile
+    if variant.stage and (rw or reads == 0):
+        # a staged read-modify-write slot would be stored into its own tile;
+        # a program that reads nothing has nothing to stage
         variant = Variant(**{**variant.__dict__, "stage": 0})
     if variant.stage:
         # the tile ring must fit the 227 KB a block can hold: shallower ring,
@@ -690,7 +691,7 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     header.append(f"#define TLK_THREADS {variant.threads}")
     if variant.stage:
         header.append(f"#define TLK_NSTAGE {variant.stage}")
-        header.append(f"#define TLK_NREAD {max(len(rord) - rord.count(-1), 1)}")
+        header.append(f"#define TLK_NREAD {len(rord) - rord.count(-1)}")
         header.append(f"#define TLK_STAGE_THREADS {variant.stage_threads}")
         header.append("#define TLK_RORD {" + ",".join(map(str, rord)) + "}")
     header.append(f"#define TLK_LDMODE {variant.ldmode}")

@@ -526,3 +526,20 @@ def test_tma_staged_batch_entry_bitwise(name, tile, reads):
         got = env_to_host(env)
         for t in targets:
             assert same_bits(got[t], host[t]), (t, host[t].shape)
+
+
+def test_programs_without_reads_at_large_n():
+    # constant fills read nothing: nothing to stage (a staged ring would wait
+    # for copies that are never issued); every size class must complete
+    from paper_1804_10120_b200.evaluator import kernel_for
+
+    src = "tensor A dim 3 rank 2;\ntensor B dim 3 rank 1;\nA(i,j) = 2.5;\nB(i) = -1.0;\n"
+    prog, vs = program(src)
+    for n in (100, (1 << 21) + 3, (1 << 22) + 256):
+        host = random_host_env(prog, n, 5)
+        env = device_env(prog, host)
+        eval_program(vs, env)
+        torch.cuda.synchronize()
+        got = env_to_host(env)
+        assert (got["A"] == 2.5).all() and (got["B"] == -1.0).all()
+    assert kernel_for(vs, env).plan.variant.stage == 0
