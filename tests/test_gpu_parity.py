@@ -543,3 +543,39 @@ def test_programs_without_reads_at_large_n():
         got = env_to_host(env)
         assert (got["A"] == 2.5).all() and (got["B"] == -1.0).all()
     assert kernel_for(vs, env).plan.variant.stage == 0
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_fuzzed_programs_large_n(seed):
+    # the fuzzed programs above at sizes past both size classes, so the
+    # default policy runs its large-N entries (the TMA-staged one for every
+    # read-only program) on odd and even point counts
+    import random
+
+    from helpers import FUZZ_DECLS, fuzz_statement
+    from paper_1804_10120_b200.evaluator import kernel_for
+    from paper_1804_10120_b200.ir import ValidationError, validate_statement
+    from paper_1804_10120_b200.parser import parse_program
+
+    rng = random.Random(5000 + seed)
+    stmts = []
+    while len(stmts) < 1 + seed % 3:
+        res = parse_program(FUZZ_DECLS + fuzz_statement(rng))
+        if not res.ok:
+            continue
+        try:
+            stmts.append(validate_statement(res.program.statements[0], res.program.decls))
+        except ValidationError:
+            continue
+    prog = parse_program(FUZZ_DECLS).program
+    n = (1 << 21) + 256 * seed + (seed % 2)
+    host = random_host_env(prog, n, seed)
+    want = {k: a.copy() for k, a in host.items()}
+    numpy_eval.eval_program(stmts, want)
+    env = device_env(prog, host)
+    eval_program(stmts, env)
+    got = env_to_host(env)
+    for k in want:
+        assert same_bits(got[k], want[k]), (k, [str(v.stmt) for v in stmts])
+    kern = kernel_for(stmts, env)
+    assert n > kern.small_n
