@@ -24,7 +24,10 @@ Additive extensions (SURVEY.md 8b "API gap"):
 * ``eval_batch(vs, envs)`` — the same statements over many independent
   subdomains in ONE launch (device domain table), bit-identical to looping
   over ``envs``;
-* ``capture_graph(fn)`` — a CUDA graph of any sequence of the above.
+* ``capture_graph(fn)`` — a CUDA graph of any sequence of the above;
+* ``bind_program(vs, env)`` / ``bind_batch(vs, envs)`` — bind once, then
+  every call is one launch with no host-side validation (the batch table of
+  C4's 512 subdomains costs 24 ms of Python per unbound ``eval_batch``).
 """
 
 from __future__ import annotations
@@ -529,15 +532,28 @@ class _BatchCache:
 _batches = _BatchCache()
 
 
-@_nvtx
-def eval_batch(vs, envs: Sequence[Env]) -> None:
-    """Execute a statement (or a program) over many independent subdomains
-    in ONE launch.  ``envs[d]`` is subdomain d's data environment; the result
-    is bitwise identical to ``for env in envs: eval_program(vs, env)``."""
-    if not isinstance(vs, (list, tuple)):
-        vs = [vs]
-    if not envs:
-        return
+# eval_batch steady state: the same list of environments, whose fields are
+# the same tensor objects as at the previous call, reuses that call's
+# uploaded table — an identity check per field instead of re-validating
+# and re-binding every subdomain (24 ms of host time for C4's 512 domains).
+_BATCH_FAST: dict = {}
+
+
+def _batch_tensors(vs, envs):
+    names = _program_names(vs)
+    out = []
+    for env in envs:
+        for nm in names:
+            f = env.get(nm) if hasattr(env, "get") else None
+            if f is None:
+                return None
+            out.append(f.data)
+    return out
+
+
+def _batch_plan(vs, envs):
+    """(kernel, table key, device) of a batchable program over `envs`, or
+    None when it must run as sequential launches."""
     table = []
     plan = kern = None
     written: set = set()
@@ -552,23 +568,113 @@ def eval_batch(vs, envs: Sequence[Env]) -> None:
         elif k is not kern:
             raise EvalError("subdomains of one batch must share field shapes and aliasing")
         if len(sizes) != 1 or any(s.where != "cuda" or s.pitch < 0 for s in stores):
-            table = None
-            break
+            return None
         for fi in wf:  # a field written by two subdomains would race
             shared_write |= stores[fi].key in written
             written.add(stores[fi].key)
         table.append((sizes.pop(), tuple((s.base, s.pitch) for s in stores), stores[0].device))
-    if table is None or shared_write or len({t[2] for t in table}) > 1:
-        for env in envs:  # not batchable: sequential launches, same bits
-            eval_program(vs, env)
-        return
+    if shared_write or len({t[2] for t in table}) > 1:
+        return None
+    return kern, tuple((t[0], t[1]) for t in table), table[0][2]
+
+
+def _batch_launch(kern, key, dev) -> None:
     import torch
 
-    dev = table[0][2]
-    key = tuple((t[0], t[1]) for t in table)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev).cuda_stream
         _batches.get(kern, key, stream).launch(stream)
+
+
+@_nvtx
+def eval_batch(vs, envs: Sequence[Env]) -> None:
+    """Execute a statement (or a program) over many independent subdomains
+    in ONE launch.  ``envs[d]`` is subdomain d's data environment; the result
+    is bitwise identical to ``for env in envs: eval_program(vs, env)``."""
+    if not isinstance(vs, (list, tuple)):
+        vs = [vs]
+    if not envs:
+        return
+    fkey = (tuple(id(v) for v in vs), id(envs))
+    hit = _BATCH_FAST.get(fkey)
+    if hit is not None and hit[0] is envs and len(envs) == hit[1]:
+        cur = _batch_tensors(vs, envs)
+        if cur is not None and len(cur) == len(hit[2]) and all(
+                a is b for a, b in zip(cur, hit[2])):
+            _batch_launch(*hit[3])
+            return
+    bp = _batch_plan(vs, envs)
+    if bp is None:
+        for env in envs:  # not batchable: sequential launches, same bits
+            eval_program(vs, env)
+        return
+    _batch_launch(*bp)
+    tensors = _batch_tensors(vs, envs)
+    if tensors is not None:
+        if len(_BATCH_FAST) > 64:
+            _BATCH_FAST.clear()
+        # holds the tensors (and the list): their ids cannot be reused
+        _BATCH_FAST[fkey] = (envs, len(envs), tensors, bp, tuple(vs))
+
+
+class Bound:
+    """A program bound to fixed field storage: calling it launches the fused
+    kernel once (one C call, no validation) on the current stream of the
+    fields' device — the host-side analogue of a CUDA graph.  Valid while no
+    bound field is resized or reallocated; results are bitwise those of
+    ``eval_program`` / ``eval_batch``."""
+
+    def __init__(self, fn, kernel: Kernel):
+        self._fn = fn
+        self.kernel = kernel
+
+    def __call__(self) -> None:
+        self._fn()
+
+
+def bind_program(vs, env: Env) -> Bound:
+    """Bind a program (fused, one gridsize) to `env`'s device fields once;
+    binding prepares the targets (resizes `=` targets) as the first
+    evaluation would, but launches nothing."""
+    if not isinstance(vs, (list, tuple)):
+        vs = [vs]
+    vs = list(vs)
+    sizes = {_prepare(v, env)[1] for v in vs}
+    if len(sizes) != 1:
+        raise EvalError("bind_program needs one gridsize for the whole program")
+    n = sizes.pop()
+    plan, kern, stores = _bind(vs, env)
+    if any(s.where != "cuda" or s.pitch < 0 for s in stores) or \
+            len({s.device for s in stores}) != 1:
+        raise EvalError("bind_program needs device fields on one GPU with uniform pitches")
+    from .runtime import address_arrays
+
+    bases, pitches = address_arrays([s.base for s in stores], [s.pitch for s in stores])
+    dev = stores[0].device
+    import torch
+
+    def go():
+        if n:
+            kern.launch_arrays(n, bases, pitches, torch.cuda.current_stream(dev).cuda_stream)
+
+    return Bound(go, kern)
+
+
+def bind_batch(vs, envs: Sequence[Env]) -> Bound:
+    """Bind a program over many subdomains once (the table is uploaded now);
+    each call is then the single batched launch of ``eval_batch``."""
+    if not isinstance(vs, (list, tuple)):
+        vs = [vs]
+    bp = _batch_plan(list(vs), envs)
+    if bp is None:
+        raise EvalError("these subdomains cannot share one launch (mixed sizes, host fields, "
+                        "several GPUs, or a field written by two subdomains)")
+    kern, key, dev = bp
+    import torch
+
+    with torch.cuda.device(dev):
+        _batches.get(kern, key, torch.cuda.current_stream(dev).cuda_stream)
+    return Bound(lambda: _batch_launch(kern, key, dev), kern)
 
 
 def capture_graph(fn, warmup: int = 1):

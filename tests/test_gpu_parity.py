@@ -579,3 +579,56 @@ def test_fuzzed_programs_large_n(seed):
         assert same_bits(got[k], want[k]), (k, [str(v.stmt) for v in stmts])
     kern = kernel_for(stmts, env)
     assert n > kern.small_n
+
+
+def test_bound_launches_and_batch_fast_path():
+    # bind_program / bind_batch launch exactly what eval_program / eval_batch
+    # would; eval_batch's steady-state path notices replaced field storage
+    from paper_1804_10120_b200 import bind_batch, bind_program
+
+    prog, vs = program(manifest()["cases"]["c4_p2"]["source"])
+    hosts, envs = [], []
+    for d in range(6):
+        host = random_host_env(prog, 300 + 2 * d, 90 + d)
+        for t in ("Gamma", "dtg"):
+            host[t][:] = 0.0
+        hosts.append(host)
+        envs.append(device_env(prog, host))
+    want = []
+    for host in hosts:
+        w = {k: a.copy() for k, a in host.items()}
+        numpy_eval.eval_program(vs, w)
+        want.append(w)
+    bound = bind_batch(vs, envs)
+    bound()
+    for env, w in zip(envs, want):
+        got = env_to_host(env)
+        for t in ("Gamma", "dtg"):
+            assert same_bits(got[t], w[t]), t
+    for env in envs:
+        for t in ("Gamma", "dtg"):
+            env[t].data.zero_()
+    eval_batch(vs, envs)          # slow path, recorded
+    eval_batch(vs, envs)          # identity fast path
+    for env, w in zip(envs, want):
+        got = env_to_host(env)
+        for t in ("Gamma", "dtg"):
+            assert same_bits(got[t], w[t]), t
+    # replace one subdomain's input storage: the fast path must rebind
+    new = random_host_env(prog, 300, 999)
+    envs[0]["Invg"].data = torch.from_numpy(new["Invg"]).cuda()
+    hosts[0]["Invg"] = new["Invg"]
+    w0 = {k: a.copy() for k, a in hosts[0].items()}
+    numpy_eval.eval_program(vs, w0)
+    eval_batch(vs, envs)
+    got = env_to_host(envs[0])
+    for t in ("Gamma", "dtg"):
+        assert same_bits(got[t], w0[t]), t
+    # single grid
+    env = envs[1]
+    env["dtg"].data.zero_()
+    env["Gamma"].data.zero_()
+    bind_program(vs, env)()
+    got = env_to_host(env)
+    for t in ("Gamma", "dtg"):
+        assert same_bits(got[t], want[1][t]), t
