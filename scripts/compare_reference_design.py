@@ -18,7 +18,13 @@ from paper_1804_10120_b200 import eval_program
 from paper_1804_10120_b200.evaluator import plan_for
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 4_000_000  # < 65535*64 (wrapper guard)
-flush = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+wbuf = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+rbuf = torch.ones(1 << 25, dtype=torch.float64, device="cuda")
+
+
+def flush():  # L2 cold and clean (bench.L2Flush)
+    wbuf.zero_()
+    rbuf.sum()
 
 
 def timed(fn, reps=21):
@@ -26,7 +32,7 @@ def timed(fn, reps=21):
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
-        flush.zero_()
+        flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
