@@ -134,3 +134,65 @@ def test_variants_compile(hoist, restrict):
     _, vs = program(manifest()["cases"]["c4_p3"]["source"])
     k = get_kernel(lower_program(vs, variant=Variant(restrict=restrict, hoist=hoist, ldmode=1)))
     assert "DFMA" not in _sass(k)
+
+
+def _defines(src: str) -> dict:
+    out = {}
+    for ln in src.splitlines():
+        if ln.startswith("#define TLK_"):
+            parts = ln.split(None, 2)
+            out[parts[1]] = parts[2] if len(parts) > 2 else ""
+    return out
+
+
+@pytest.mark.parametrize("name,tile,staged", [("c1_dtg", 256, 8), ("c3_christoffel", 256, 18),
+                                              ("c4_p2", 256, 34), ("c4_p3", 256, 32)])
+def test_staged_policy_ring_layout(name, tile, staged):
+    # choose_variant's staged share, and the ring's read-slot ordinals: the
+    # first `staged` read slots in slot order, numbered densely
+    _, vs = program(manifest()["cases"][name]["source"])
+    plan = lower_program(vs)
+    var = plan.variant
+    assert var.stage == 3 and var.stage_threads == tile
+    d = _defines(plan.source)
+    rord = [int(x) for x in d["TLK_RORD"].strip("{}").split(",")]
+    assert int(d["TLK_NREAD"]) == staged == sum(1 for r in rord if r >= 0)
+    reads = [j for j, fl in enumerate(plan.slot_flags) if fl & SLOT_READ]
+    assert [rord[j] for j in reads[:staged]] == list(range(staged))
+    assert all(rord[j] == -1 for j in range(len(rord)) if j not in reads[:staged])
+    assert 3 * staged * tile * 8 <= 224 * 1024
+    assert int(d["TLK_STAGE_THREADS"]) == tile and int(d["TLK_THREADS"]) == 256
+
+
+def test_stage_refused_for_read_write_and_read_free_programs():
+    from paper_1804_10120_b200.lowering import Variant
+
+    _, vs = program("tensor A dim 3 rank 1;\ntensor B dim 3 rank 1;\nA(i) += B(i);\n")
+    assert lower_program(vs, variant=Variant(stage=3)).variant.stage == 0
+    _, vs = program("tensor A dim 3 rank 2;\nA(i,j) = 1.5;\n")
+    plan = lower_program(vs, variant=Variant(stage=3))
+    assert plan.variant.stage == 0 and "#define TLK_NSTAGE" not in plan.source
+
+
+def test_stage_ring_clamped_to_shared_memory():
+    # 4 x 256-point tiles of 64 reads would need 512 KB: depth, then tile,
+    # shrink until the ring fits the 224 KB budget
+    from paper_1804_10120_b200.lowering import STAGE_SMEM_MAX, Variant
+
+    _, vs = program(manifest()["cases"]["c4_p3"]["source"])
+    plan = lower_program(vs, variant=Variant(stage=4, stage_threads=256))
+    var = plan.variant
+    assert var.stage >= 2
+    assert var.stage * plan.reads * var.stage_threads * 8 <= STAGE_SMEM_MAX
+
+
+@pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="no cuobjdump")
+def test_staged_entries_use_bulk_copies_without_spills():
+    _, vs = program(manifest()["cases"]["c4_p2"]["source"])
+    k = get_kernel(lower_program(vs))
+    sass = _sass(k)
+    assert "tlk_stage_v1" in sass and "tlk_stage_batch_v1" in sass
+    assert "UBLKCP" in sass  # cp.async.bulk (TMA engine)
+    assert "SYNCS" in sass  # mbarrier operations
+    assert "LDL" not in sass and "STL" not in sass
+    assert "DFMA" not in sass
