@@ -1,6 +1,6 @@
 #!/bin/bash
 # partially staged policy: parity suite, smoke, bench (both arms), sweep, small-N, ncu of the bench kernel
-TAG=${1:-r01z}
+TAG=${1:-r01final}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 export PYTHONPATH=$PWD
