@@ -307,8 +307,9 @@ tlk_stage_v1(const tlk_flat_params prm) {
 // dedicated producer warp (block = TLK_STAGE_THREADS consumers + 32).  Work
 // items are (domain, tile) pairs, built on the host at tlb_batch_create:
 // items[w] = {domain | count << 32, first point}.  Per item the producer warp
-// reads the domain's slot pointers from the batch table into the stage's
-// pointer block (lanes stride over slots), then lane 0 issues the bulk
+// fetches the record and the domain's slot pointers one item ahead into
+// registers (lanes stride over slots), writes them to the stage's pointer
+// block once the stage is free, then lane 0 issues the bulk
 // copies of the staged read slots (full[s] completes on their bytes plus 32
 // lane arrivals).  Tiles with an odd count or any slot not 16-byte aligned
 // are not copied: their count is stored negated and consumers read every
@@ -346,25 +347,46 @@ tlk_stage_batch_v1(const long long* __restrict__ table, const longlong2* __restr
   }
   __syncthreads();
   if (tid >= kTile) {  // producer warp
+    // item records and slot pointers are fetched one item ahead, into
+    // registers, so their latency overlaps the wait for a free stage
+    constexpr int kPer = (TLK_NSLOTS + 31) / 32;
     const int lane = tid - kTile;
+    double* pre[kPer];
+    long long pd = 0, pbase = 0;
+    int pcnt = 0;
+    auto fetch = [&](long long w) {
+      const longlong2 item = items[w];
+      pd = item.x & 0xffffffffLL;
+      pcnt = (int)(item.x >> 32);
+      pbase = item.y;
+      const long long* rec = table + pd * (TLK_NSLOTS + 1);
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int j = lane + 32 * q;
+        pre[q] = j < TLK_NSLOTS ? reinterpret_cast<double*>(__ldg(rec + 1 + j)) + pbase
+                                : nullptr;
+      }
+    };
+    if (blockIdx.x < nitems) fetch(blockIdx.x);
     int k = 0;
     for (long long w = blockIdx.x; w < nitems; w += gridDim.x, ++k) {
       const int s = k % TLK_NSTAGE;
       if (k >= TLK_NSTAGE)
         tlk_mbar_wait(tlk_smem_addr(&empty[s]), (unsigned)(k / TLK_NSTAGE - 1) & 1u);
-      const longlong2 item = items[w];
-      const long long d = item.x & 0xffffffffLL;
-      const int cnt = (int)(item.x >> 32);
-      const long long* rec = table + d * (TLK_NSLOTS + 1);
+      const int cnt = pcnt;
       bool ok = (cnt & 1) == 0;
-      for (int j = lane; j < TLK_NSLOTS; j += 32) {
-        double* g = reinterpret_cast<double*>(__ldg(rec + 1 + j)) + item.y;
-        ok = ok && (reinterpret_cast<unsigned long long>(g) & 15ull) == 0;
-        ptrs[s * TLK_NSLOTS + j] = g;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int j = lane + 32 * q;
+        if (j < TLK_NSLOTS) {
+          ok = ok && (reinterpret_cast<unsigned long long>(pre[q]) & 15ull) == 0;
+          ptrs[s * TLK_NSLOTS + j] = pre[q];
+        }
       }
       ok = __all_sync(0xffffffffu, ok);
       if (lane == 0) cnts[s] = ok ? cnt : -cnt;
       __syncwarp();
+      if (w + gridDim.x < nitems) fetch(w + gridDim.x);  // next item, in flight
       const unsigned fb = tlk_smem_addr(&full[s]);
       if (ok && lane == 0) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
