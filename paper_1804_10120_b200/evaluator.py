@@ -551,6 +551,20 @@ def _batch_tensors(vs, envs):
     return out
 
 
+def _device_groups(vs, envs) -> dict:
+    """Subdomain indices per CUDA device, in order of first appearance (a
+    subdomain's device is its LHS field's; host-resident ones group under
+    None)."""
+    groups: dict = {}
+    lhs = vs[0].stmt.lhs.field
+    for i, env in enumerate(envs):
+        f = env.get(lhs) if hasattr(env, "get") else None
+        d = getattr(getattr(f, "data", None), "device", None)
+        key = d if getattr(d, "type", None) == "cuda" else None
+        groups.setdefault(key, []).append(i)
+    return groups
+
+
 def _batch_plan(vs, envs):
     """(kernel, table key, device) of a batchable program over `envs`, or
     None when it must run as sequential launches."""
@@ -603,6 +617,13 @@ def eval_batch(vs, envs: Sequence[Env]) -> None:
                 a is b for a, b in zip(cur, hit[2])):
             _batch_launch(*hit[3])
             return
+    groups = _device_groups(vs, envs)
+    if len(groups) > 1:
+        # subdomains spread over several GPUs of this process: one batched
+        # launch per GPU (asynchronous, so the GPUs run concurrently)
+        for idx in groups.values():
+            eval_batch(vs, [envs[i] for i in idx])
+        return
     bp = _batch_plan(vs, envs)
     if bp is None:
         for env in envs:  # not batchable: sequential launches, same bits

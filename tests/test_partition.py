@@ -94,3 +94,24 @@ def test_two_rank_gloo_partition_and_norm():
     numpy_eval.eval_program(vs, host)
     want = np.sqrt((host["Gamma"] ** 2).sum() + (host["dtg"] ** 2).sum())
     assert n0 == pytest.approx(want, rel=1e-12)
+
+
+def test_batch_subdomains_grouped_per_device():
+    # eval_batch issues one batched launch per GPU of the process; the
+    # grouping keeps first-appearance order and each device's domain order
+    from collections import namedtuple
+    from types import SimpleNamespace
+
+    from paper_1804_10120_b200.evaluator import _device_groups
+
+    Dev = namedtuple("Dev", "type index")  # hashable like torch.device
+
+    def env(dev):
+        dv = Dev("cuda", dev) if dev is not None else Dev("cpu", None)
+        return {"T": SimpleNamespace(data=SimpleNamespace(device=dv))}
+
+    v = SimpleNamespace(stmt=SimpleNamespace(lhs=SimpleNamespace(field="T")))
+    envs = [env(1), env(0), env(1), env(None), env(0)]
+    groups = _device_groups([v], envs)
+    assert list(groups.values()) == [[0, 2], [1, 4], [3]]
+    assert len(_device_groups([v], [env(0), env(0)])) == 1
