@@ -1,0 +1,85 @@
+"""Soak test of the staged entries: random programs (the fuzz generator of
+tests/helpers.py), random sizes (log-uniform, 1 .. 2^22 points) and random
+ring shapes (depth 2-4, tiles 64-256, any staged share), each result checked
+bitwise — against the CPU oracle up to 2^18 points, above that against the
+plain flat entry of the same program.  Runs for --seconds and prints one
+JSON summary line.
+Usage: PYTHONPATH=.:tests python scripts/soak.py [--seconds 300]"""
+
+import argparse
+import json
+import random
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+
+from helpers import FUZZ_DECLS, device_env, env_to_host, fuzz_statement, random_host_env, same_bits  # noqa: E402
+from oracle import numpy_eval  # noqa: E402
+from paper_1804_10120_b200.evaluator import _bind  # noqa: E402
+from paper_1804_10120_b200.ir import ValidationError, validate_statement  # noqa: E402
+from paper_1804_10120_b200.lowering import Variant, lower_program  # noqa: E402
+from paper_1804_10120_b200.parser import parse_program  # noqa: E402
+from paper_1804_10120_b200.runtime import Kernel  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--seconds", type=float, default=300)
+ap.add_argument("--seed", type=int, default=7)
+args = ap.parse_args()
+rng = random.Random(args.seed)
+prog = parse_program(FUZZ_DECLS).program
+stats = {"cases": 0, "staged": 0, "oracle_checked": 0, "flat_checked": 0, "mismatches": []}
+t_end = time.time() + args.seconds
+stream = torch.cuda.current_stream().cuda_stream
+
+
+def run(stmts, env, variant, n):
+    _, _, stores = _bind(stmts, env)
+    k = Kernel(lower_program(stmts, variant=variant))
+    k.launch(n, [s.base for s in stores], [s.pitch for s in stores], stream)
+    torch.cuda.synchronize()
+    return k
+
+
+while time.time() < t_end:
+    stmts = []
+    while len(stmts) < rng.randint(1, 3):
+        res = parse_program(FUZZ_DECLS + fuzz_statement(rng))
+        if not res.ok:
+            continue
+        try:
+            stmts.append(validate_statement(res.program.statements[0], res.program.decls))
+        except ValidationError:
+            continue
+    n = int(2 ** rng.uniform(0, 22))
+    var = Variant(stage=rng.choice([2, 3, 4]), stage_threads=rng.choice([64, 128, 256]),
+                  stage_reads=rng.choice([0, 1, 2, 5, 9, 17]), hoist=rng.random() < 0.5)
+    if lower_program(stmts, variant=var).variant.stage == 0 and rng.random() < 0.85:
+        continue  # mostly programs the staged entry can take (no read-write slot)
+    host = random_host_env(prog, n, rng.randrange(1 << 30))
+    env = device_env(prog, host)
+    k = run(stmts, env, var, n)
+    got = env_to_host(env)
+    stats["cases"] += 1
+    stats["staged"] += int(k.vec == 3)
+    if n <= 1 << 18:
+        want = {key: a.copy() for key, a in host.items()}
+        numpy_eval.eval_program(stmts, want)
+        stats["oracle_checked"] += 1
+    else:
+        env2 = device_env(prog, host)
+        run(stmts, env2, Variant(), n)
+        want = env_to_host(env2)
+        stats["flat_checked"] += 1
+    for key in want:
+        if not same_bits(got[key], want[key]):
+            stats["mismatches"].append({"n": n, "variant": var.tag(), "field": key,
+                                        "stmts": [str(v.stmt) for v in stmts]})
+            break
+    del env
+print(json.dumps(stats))
