@@ -297,6 +297,10 @@ def run_ours(args, dist: Dist) -> dict | None:
         cpu = cpu_baseline(args)
         port = cpu_port_baseline(args)
 
+    nsweep = None
+    if not args.no_configs:
+        nsweep = run_n_sweep(dist)
+
     configs = None
     if not args.no_configs and dist.world == 1:
         configs = run_configs()
@@ -357,9 +361,56 @@ def run_ours(args, dist: Dist) -> dict | None:
         "cpu_baseline": cpu,
         "cpu_baseline_numpy_port": port,
         "configs": configs,
+        "n_sweep": nsweep,
         "clocks": clk,
         "gpu_launches": launches,
     }
+
+
+def run_n_sweep(dist: Dist) -> dict:
+    """Throughput vs total grid size at this run's GPU count (the metric's
+    "vs N" at 1/2/4/8 B200): C2 Maxwell at 10^6..10^8 and P2 at 2^21..2^26
+    points in total, split into per-rank slabs like the headline; eager
+    launches, per-rank CUDA events, max over ranks."""
+    import torch
+
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200 import eval_program
+    from paper_1804_10120_b200.evaluator import plan_for
+
+    out = {}
+    for name, totals in (("c2_maxwell", (10**6, 10**7, 10**8)),
+                         ("p2", (1 << 21, 1 << 24, 1 << 26))):
+        prog, vs = tb.load(tb.PROGRAMS[name])
+        targets = {v.stmt.lhs.field for v in vs}
+        for total in totals:
+            lo, hi = slab(total, dist.rank, dist.world)
+            env = tb.make_env(prog, "__none__", 0, SEED)
+            for f in env.values():
+                f.resize(hi - lo)
+                if f.name not in targets:
+                    f.data.uniform_()
+            k = 10 if total <= 1 << 24 else 5
+            for _ in range(3):
+                eval_program(vs, env)
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(k):
+                eval_program(vs, env)
+            b.record()
+            b.synchronize()
+            t = dist.allreduce(a.elapsed_time(b) / 1e3 / k, "max")
+            bpp = plan_for(vs, env).bytes_per_point
+            out[f"{name}_{total}"] = {"points_total": total, "points_per_gpu": hi - lo,
+                                      "us": round(t * 1e6, 2), "gridpoints_per_s": total / t,
+                                      "hbm_gbs_total": bpp * total / t / 1e9}
+            del env
+            torch.cuda.empty_cache()
+    out["method"] = ("total points split into per-rank slabs; 3 warm-up then 5-10 eager "
+                     "back-to-back launches per rank timed with CUDA events, max over ranks")
+    return out
 
 
 def run_e2e(args, dist: Dist, vs, n_local: int) -> dict:
