@@ -632,3 +632,37 @@ def test_bound_launches_and_batch_fast_path():
     got = env_to_host(env)
     for t in ("Gamma", "dtg"):
         assert same_bits(got[t], want[1][t]), t
+
+
+def test_staged_main_loop_special_values():
+    # IEEE specials (inf, nan payloads, signed zeros, subnormals) through the
+    # staged entry's ring — golden inputs tiled past many whole tiles — must
+    # give the plain entry's bits, which the golden vectors pin
+    from paper_1804_10120_b200.evaluator import _bind
+    from paper_1804_10120_b200.lowering import Variant, lower_program
+    from paper_1804_10120_b200.runtime import Kernel
+
+    case = manifest()["cases"]["special_values"]
+    prog, vs = program(case["source"])
+    host, _ = golden_io("special_values")
+    n0 = host["w"].shape[-1]
+    reps = (1 << 20) // n0 + 3
+    big = {k: np.ascontiguousarray(np.concatenate([a] * reps, axis=-1)) for k, a in host.items()}
+    specials = np.array([np.inf, -np.inf, np.nan, -0.0, 0.0, 5e-324, -5e-324, 1e308, -1e-310],
+                        dtype=np.float64)
+    big["w"][: specials.size] = specials
+    big["B"][..., -specials.size:] = specials
+    n = big["w"].shape[-1]
+    outs = []
+    for var in (Variant(), Variant(stage=3, stage_threads=256), Variant(stage=2, stage_reads=1)):
+        env = device_env(prog, big)
+        _, _, stores = _bind(vs, env)
+        k = Kernel(lower_program(vs, variant=var))
+        k.launch(n, [s.base for s in stores], [s.pitch for s in stores],
+                 torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        outs.append(env_to_host(env)["A"])
+    assert same_bits(outs[0], outs[1]) and same_bits(outs[0], outs[2])
+    want = {k: a.copy() for k, a in big.items()}
+    numpy_eval.eval_program(vs, want)
+    assert same_bits(outs[0], want["A"])
