@@ -25,7 +25,7 @@ from paper_1804_10120_b200.evaluator import _bind  # noqa: E402
 from paper_1804_10120_b200.ir import ValidationError, validate_statement  # noqa: E402
 from paper_1804_10120_b200.lowering import Variant, lower_program  # noqa: E402
 from paper_1804_10120_b200.parser import parse_program  # noqa: E402
-from paper_1804_10120_b200.runtime import Kernel  # noqa: E402
+from paper_1804_10120_b200.runtime import Batch, Kernel  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--seconds", type=float, default=300)
@@ -33,7 +33,8 @@ ap.add_argument("--seed", type=int, default=7)
 args = ap.parse_args()
 rng = random.Random(args.seed)
 prog = parse_program(FUZZ_DECLS).program
-stats = {"cases": 0, "staged": 0, "oracle_checked": 0, "flat_checked": 0, "mismatches": []}
+stats = {"cases": 0, "staged": 0, "oracle_checked": 0, "flat_checked": 0, "batch_cases": 0,
+         "mismatches": []}
 t_end = time.time() + args.seconds
 stream = torch.cuda.current_stream().cuda_stream
 
@@ -56,6 +57,34 @@ while time.time() < t_end:
             stmts.append(validate_statement(res.program.statements[0], res.program.decls))
         except ValidationError:
             continue
+    if rng.random() < 0.3:
+        # multi-domain batch (plain or staged batch entry) vs the oracle
+        var = Variant(stage=rng.choice([0, 2, 3]), stage_threads=rng.choice([64, 128, 256]),
+                      stage_reads=rng.choice([0, 1, 3]), batch_vec=rng.choice([1, 2, 3]),
+                      batch_threads=rng.choice([0, 64, 128]))
+        sizes = [int(2 ** rng.uniform(0, 13)) for _ in range(rng.randint(1, 40))]
+        hosts = [random_host_env(prog, m, rng.randrange(1 << 30)) for m in sizes]
+        envs = [device_env(prog, h) for h in hosts]
+        k = Kernel(lower_program(stmts, variant=var))
+        bases, pitches = [], []
+        for env in envs:
+            _, _, stores = _bind(stmts, env)
+            bases.append([st.base for st in stores])
+            pitches.append([st.pitch for st in stores])
+        Batch(k, bases, pitches, sizes, stream).launch(stream)
+        torch.cuda.synchronize()
+        stats["batch_cases"] += 1
+        for env, h in zip(envs, hosts):
+            want = {key: a.copy() for key, a in h.items()}
+            numpy_eval.eval_program(stmts, want)
+            got = env_to_host(env)
+            bad = [key for key in want if not same_bits(got[key], want[key])]
+            if bad:
+                stats["mismatches"].append({"batch": True, "sizes": sizes, "variant": var.tag(),
+                                            "field": bad[0],
+                                            "stmts": [str(v.stmt) for v in stmts]})
+                break
+        continue
     n = int(2 ** rng.uniform(0, 22))
     var = Variant(stage=rng.choice([2, 3, 4]), stage_threads=rng.choice([64, 128, 256]),
                   stage_reads=rng.choice([0, 1, 2, 5, 9, 17]), hoist=rng.random() < 0.5)
