@@ -544,7 +544,9 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
     arrays = reads + writes
     # the staged entries unroll per-slot loops: beyond a few hundred slots
     # (unmeasured territory, slow NVRTC compiles) the plain entries are used
-    stageable = rw_slots == 0 and arrays <= STAGE_MAX_SLOTS
+    # write-dominated programs stream better through the plain entries
+    # (outer products, copies: -3..-13 % staged, profiles/r01/tune_suite.jsonl)
+    stageable = rw_slots == 0 and arrays <= STAGE_MAX_SLOTS and reads > writes
     if n_ops <= 1.5 * arrays:
         if not stageable:
             return Variant(restrict=True, hoist=False, ldmode=0, vec=1, waves=4,
@@ -566,6 +568,17 @@ STAGE_SMEM_MAX = 224 * 1024
 
 # largest program (read + written component arrays) the policy stages
 STAGE_MAX_SLOTS = 256
+# fewest resident warps per SM the policy accepts for a staged ring
+STAGE_MIN_WARPS = 8
+
+
+def _stage_warps(variant: "Variant", staged: int) -> int:
+    """Warps per SM the staged entry can keep resident: blocks limited by the
+    ring's shared memory (228 KB per SM, ~1 KB reserved per block) and by
+    2048 threads per SM."""
+    ring = variant.stage * max(staged, 1) * variant.stage_threads * 8
+    blocks = min(228 * 1024 // (ring + 1024), 2048 // variant.stage_threads)
+    return blocks * variant.stage_threads // 32
 
 # size classes (Variant.small_class): largest launch, in points, that still
 # runs the small-N choices — the crossovers in profiles/r01/tune_cross.jsonl
@@ -641,6 +654,7 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     writes = sum(1 for f in b.slot_flags if f & SLOT_WRITE)
     rw = sum(1 for f in b.slot_flags if f == SLOT_READ | SLOT_WRITE)
     phases = _phases(b.instrs)
+    policy = variant is None
     if variant is None:
         variant = _env_variant(choose_variant(reads, writes, n_ops, rw, b.chained))
         if "TLK_STAGE_FRAC" in os.environ:  # tuning: staged share of the read slots
@@ -668,6 +682,10 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         if (depth, tile) != (variant.stage, variant.stage_threads):
             variant = Variant(**{**variant.__dict__, "stage": depth if depth >= 2 else 0,
                                  "stage_threads": tile})
+        if policy and variant.stage and _stage_warps(variant, staged) < STAGE_MIN_WARPS:
+            # a ring this large leaves too few warps per SM to consume it
+            # (contract1, 90 reads: 4 warps, -13 %, profiles/r01/tune_suite.jsonl)
+            variant = Variant(**{**variant.__dict__, "stage": 0})
     rord: list[int] = []
     if variant.stage:
         # TMA-staged entry: the first `stage_reads` read slots (all by
