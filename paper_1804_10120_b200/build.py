@@ -65,7 +65,11 @@ def precompile(sources: dict[str, str]) -> dict[str, dict]:
             raise RuntimeError(f"{name}: {res.diagnostics}")
         prog = res.program
         vs = [validate_statement(s, prog.decls) for s in prog.statements]
-        plans = [lower_program(vs)] + ([lower_program([v]) for v in vs] if len(vs) > 1 else [])
+        try:
+            plans = [lower_program(vs)] + ([lower_program([v]) for v in vs] if len(vs) > 1
+                                           else [])
+        except ArithmeticError:
+            continue  # a literal `1/0` (raises at run time, like the reference): nothing to build
         for p in plans:
             k: Kernel = get_kernel(p)
         out[name] = {"slots": plans[0].n_slots, "bytes_per_point": plans[0].bytes_per_point,

@@ -66,6 +66,8 @@ struct Driver {
   CUresult (*EventRecord)(CUevent, CUstream) = nullptr;
   CUresult (*EventDestroy)(CUevent) = nullptr;
   CUresult (*ModuleLoadData)(CUmodule*, const void*) = nullptr;
+  CUresult (*ModuleUnload)(CUmodule) = nullptr;
+  CUresult (*CtxSynchronize)(void) = nullptr;
   CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
   CUresult (*FuncGetAttribute)(int*, CUfunction_attribute, CUfunction) = nullptr;
   CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
@@ -151,6 +153,8 @@ int load_driver_locked() {
             bind(h, g_cu.EventRecord, "cuEventRecord") &&
             bind(h, g_cu.EventDestroy, "cuEventDestroy_v2") &&
             bind(h, g_cu.ModuleLoadData, "cuModuleLoadData") &&
+            bind(h, g_cu.ModuleUnload, "cuModuleUnload") &&
+            bind(h, g_cu.CtxSynchronize, "cuCtxSynchronize") &&
             bind(h, g_cu.ModuleGetFunction, "cuModuleGetFunction") &&
             bind(h, g_cu.FuncGetAttribute, "cuFuncGetAttribute") &&
             bind(h, g_cu.FuncSetAttribute, "cuFuncSetAttribute") &&
@@ -458,7 +462,22 @@ int tlb_kernel_cubin(const tlb_kernel* k, const void** data, long long* size) {
   return 0;
 }
 
-void tlb_kernel_destroy(tlb_kernel* k) { delete k; }  // modules live until process exit
+void tlb_kernel_destroy(tlb_kernel* k) {
+  if (!k) return;
+  if (g_driver_ok && !k->loaded.empty()) {
+    // unload the module from every context it was loaded into, after that
+    // context's pending work (a launch of it may still be queued)
+    CUcontext cur = nullptr;
+    g_cu.CtxGetCurrent(&cur);
+    for (auto& kv : k->loaded) {
+      if (g_cu.CtxSetCurrent(kv.first) != CUDA_SUCCESS) continue;
+      g_cu.CtxSynchronize();
+      g_cu.ModuleUnload(kv.second.mod);
+    }
+    g_cu.CtxSetCurrent(cur);
+  }
+  delete k;
+}
 
 int tlb_kernel_set_slots(tlb_kernel* k, int nfields, int nslots, const int* slot_field,
                          const long long* slot_comp, const int* slot_flags) {
@@ -679,6 +698,7 @@ void tlb_batch_destroy(tlb_batch* b) {
     CUcontext cur = nullptr;
     g_cu.CtxGetCurrent(&cur);
     if (cur != b->ctx) g_cu.CtxSetCurrent(b->ctx);
+    g_cu.CtxSynchronize();  // a queued batch launch may still read the table
     g_cu.MemFree(b->table);
     if (b->items) g_cu.MemFree(b->items);
     if (cur && cur != b->ctx) g_cu.CtxSetCurrent(cur);

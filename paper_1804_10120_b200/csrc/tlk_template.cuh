@@ -33,6 +33,12 @@
 #ifndef TLK_THREADS
 #define TLK_THREADS 256
 #endif
+// Minimum resident blocks per SM the flat entries are compiled for (the
+// second __launch_bounds__ argument: caps registers so a launch that is one
+// wave at this occupancy never spills into a second, partial wave).
+#ifndef TLK_MINB
+#define TLK_MINB 1
+#endif
 // Unroll factor of the grid-stride loops (1 = one point group per trip; the
 // per-point body already exposes all of its loads, occupancy does the rest).
 #ifndef TLK_UNROLL
@@ -75,9 +81,22 @@ template <> __device__ __forceinline__ double2 tl_splat<double2>(double c) { ret
 #endif
 // TLK_STMODE 0: st.global.cs (streaming)            [default]
 //            1: plain st.global
+//            2: st.global.L1::no_allocate
 #ifndef TLK_STMODE
 #define TLK_STMODE 0
 #endif
+
+// TLK_L2HINT 1: the read-only loads (mode 1) and the staged entry's bulk
+//               copies carry an L2 evict-first cache policy (every input byte
+//               is read exactly once)                        [tuning knob]
+#ifndef TLK_L2HINT
+#define TLK_L2HINT 0
+#endif
+__device__ __forceinline__ unsigned long long tl_evict_first_policy() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 
 // LD is a template parameter so one module can hold entries with different
 // load flavours (the staged entry reads its tiles with mode 3).
@@ -88,7 +107,12 @@ __device__ __forceinline__ T tl_ld(const double* p) {
       return __ldcs(p);
     } else if constexpr (LD == 1) {
       double v;
+#if TLK_L2HINT
+      asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+          : "=d"(v) : "l"(p), "l"(tl_evict_first_policy()));
+#else
       asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+#endif
       return v;
     } else {
       return *p;
@@ -98,7 +122,12 @@ __device__ __forceinline__ T tl_ld(const double* p) {
       return __ldcs(reinterpret_cast<const double2*>(p));
     } else if constexpr (LD == 1) {
       double2 v;
+#if TLK_L2HINT
+      asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+          : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(tl_evict_first_policy()));
+#else
       asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+#endif
       return v;
     } else {
       return *reinterpret_cast<const double2*>(p);
@@ -109,6 +138,8 @@ __device__ __forceinline__ T tl_ld(const double* p) {
 __device__ __forceinline__ void tl_st(double* p, double v) {
 #if TLK_STMODE == 0
   __stcs(p, v);
+#elif TLK_STMODE == 2
+  asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 #else
   *p = v;
 #endif
@@ -116,6 +147,9 @@ __device__ __forceinline__ void tl_st(double* p, double v) {
 __device__ __forceinline__ void tl_st(double* p, double2 v) {
 #if TLK_STMODE == 0
   __stcs(reinterpret_cast<double2*>(p), v);
+#elif TLK_STMODE == 2
+  asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y)
+               : "memory");
 #else
   *reinterpret_cast<double2*>(p) = v;
 #endif
@@ -134,7 +168,7 @@ struct tlk_shared_ptrs {
   double* const* p;
 };
 
-extern "C" __global__ void __launch_bounds__(TLK_THREADS)
+extern "C" __global__ void __launch_bounds__(TLK_THREADS, TLK_MINB)
 tlk_flat_v1(const tlk_flat_params prm) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   TLK_LOOP
@@ -142,7 +176,7 @@ tlk_flat_v1(const tlk_flat_params prm) {
     tlk_point<double>(prm, x);
 }
 
-extern "C" __global__ void __launch_bounds__(TLK_THREADS)
+extern "C" __global__ void __launch_bounds__(TLK_THREADS, TLK_MINB)
 tlk_flat_v2(const tlk_flat_params prm) {
   const long long pairs = prm.n >> 1;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -233,6 +267,9 @@ tlk_batch_v2(const long long* __restrict__ table, int ndom) {
 // TLK_STAGE_THREADS and the per-slot read ordinals TLK_RORD); needs every
 // read slot 16-byte aligned (the runtime checks).
 #ifdef TLK_NSTAGE
+#ifndef TLK_TILE_ORDER
+#define TLK_TILE_ORDER 0
+#endif
 #if TLK_NREAD < 1
 #error "a staged kernel needs at least one staged read slot (its mbarrier would never complete)"
 #endif
@@ -248,6 +285,16 @@ tlk_stage_v1(const tlk_flat_params prm) {
   __shared__ __align__(8) unsigned long long bar[TLK_NSTAGE];
   const long long ntiles = prm.n / kTile;
   const int tid = threadIdx.x;
+  // tile order: 0 = interleaved (block b takes b, b + grid, ...), so the
+  // blocks sweep the grid together; 1 = one contiguous run of tiles per block
+#if TLK_TILE_ORDER == 1
+  const long long per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const long long t0 = (long long)blockIdx.x * per;
+  const long long t1 = ntiles < t0 + per ? ntiles : t0 + per;
+  const long long tstep = 1;
+#else
+  const long long t0 = blockIdx.x, t1 = ntiles, tstep = gridDim.x;
+#endif
   if (tid == 0) {
     for (int s = 0; s < TLK_NSTAGE; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tlk_smem_addr(&bar[s])));
@@ -258,24 +305,36 @@ tlk_stage_v1(const tlk_flat_params prm) {
     const unsigned b = tlk_smem_addr(&bar[s]);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                  ::"r"(b), "r"((unsigned)(TLK_NREAD * kTile * sizeof(double))) : "memory");
+#if TLK_L2HINT
+    const unsigned long long pol = tl_evict_first_policy();
+#endif
 #pragma unroll
     for (int j = 0; j < TLK_NSLOTS; ++j) {
       if (kRord[j] < 0) continue;
       const double* src = prm.p[j] + t * kTile;
       double* dst = tlk_sm + ((long long)s * TLK_NREAD + kRord[j]) * kTile;
+#if TLK_L2HINT
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+          "[%0], [%1], %2, [%3], %4;"
+          ::"r"(tlk_smem_addr(dst)), "l"(src), "r"((unsigned)(kTile * sizeof(double))), "r"(b),
+            "l"(pol)
+          : "memory");
+#else
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
           ::"r"(tlk_smem_addr(dst)), "l"(src), "r"((unsigned)(kTile * sizeof(double))), "r"(b)
           : "memory");
+#endif
     }
   };
   if (tid == 0)
     for (int s = 0; s < TLK_NSTAGE; ++s) {
-      const long long t = blockIdx.x + (long long)s * gridDim.x;
-      if (t < ntiles) issue(t, s);
+      const long long t = t0 + (long long)s * tstep;
+      if (t < t1) issue(t, s);
     }
   int it = 0;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+  for (long long t = t0; t < t1; t += tstep, ++it) {
     const int s = it % TLK_NSTAGE;
     const unsigned phase = (unsigned)(it / TLK_NSTAGE) & 1u;
     const unsigned b = tlk_smem_addr(&bar[s]);
@@ -293,8 +352,8 @@ tlk_stage_v1(const tlk_flat_params prm) {
     tlk_point<double, 3>(q, tid);
     __syncthreads();  // every thread is done with stage s
     if (tid == 0) {
-      const long long tn = t + (long long)TLK_NSTAGE * gridDim.x;
-      if (tn < ntiles) issue(tn, s);
+      const long long tn = t + (long long)TLK_NSTAGE * tstep;
+      if (tn < t1) issue(tn, s);
     }
   }
   const long long stride = (long long)gridDim.x * blockDim.x;

@@ -33,6 +33,7 @@ Additive extensions (SURVEY.md 8b "API gap"):
 from __future__ import annotations
 
 import threading
+from collections import OrderedDict
 from typing import Any, Mapping, Sequence
 
 import numpy as np
@@ -121,7 +122,40 @@ def _is_tensor_field(f) -> bool:
     return hasattr(f, "shape") and hasattr(f, "data") and getattr(f.data, "ndim", 0) == 3
 
 
-_NAMES: dict[int, tuple] = {}
+class _LRU:
+    """Bounded, thread-safe mapping with least-recently-used eviction: the
+    host-side caches below key on statement identities and pin what they
+    key on, so in a long-running process that keeps generating statements
+    they must not grow without bound (VERDICT r01 weak #8)."""
+
+    def __init__(self, cap: int) -> None:
+        self.cap = cap
+        self._d: OrderedDict = OrderedDict()
+        self._lock = threading.Lock()
+
+    def get(self, key):
+        with self._lock:
+            hit = self._d.get(key)
+            if hit is not None:
+                self._d.move_to_end(key)
+            return hit
+
+    def put(self, key, value) -> None:
+        with self._lock:
+            self._d[key] = value
+            self._d.move_to_end(key)
+            while len(self._d) > self.cap:
+                self._d.popitem(last=False)
+
+    def __len__(self) -> int:
+        return len(self._d)
+
+    def clear(self) -> None:
+        with self._lock:
+            self._d.clear()
+
+
+_NAMES = _LRU(4096)
 
 
 def _rhs_names(v) -> list[str]:
@@ -129,7 +163,7 @@ def _rhs_names(v) -> list[str]:
     if hit is not None and hit[0] is v:
         return hit[1]
     out = _rhs_names_walk(v)
-    _NAMES[id(v)] = (v, out)
+    _NAMES.put(id(v), (v, out))
     return out
 
 
@@ -248,9 +282,8 @@ def _f64():
 
 
 class _PlanCache:
-    def __init__(self) -> None:
-        self._d: dict = {}
-        self._lock = threading.Lock()
+    def __init__(self, cap: int = 1024) -> None:
+        self._d = _LRU(cap)
 
     def get(self, vs: Sequence[Any], alias: tuple, components=None) -> tuple[KernelPlan, Kernel]:
         key = (tuple(id(v) for v in vs), alias, components)
@@ -263,8 +296,7 @@ class _PlanCache:
         except LoweringError as exc:
             raise EvalError(str(exc)) from exc
         kern = get_kernel(plan)
-        with self._lock:
-            self._d[key] = (tuple(vs), plan, kern)  # keeps vs alive: ids stay unique
+        self._d.put(key, (tuple(vs), plan, kern))  # keeps vs alive: ids stay unique
         return plan, kern
 
 
@@ -287,7 +319,10 @@ def _bind(vs: Sequence[Any], env: Env, components=None):
     for n in names:
         d = fields[n].data
         host_np = isinstance(d, np.ndarray)
-        key = (d.ctypes.data if host_np else d.data_ptr(), tuple(d.shape))
+        # same address, shape AND strides: a transposed/permuted view of the
+        # same buffer is a different field (and then fails _check_disjoint)
+        key = ((d.ctypes.data, tuple(d.shape), tuple(d.strides)) if host_np
+               else (d.data_ptr(), tuple(d.shape), tuple(d.stride())))
         size = d.size if host_np else d.numel()
         if key[0] and size:
             r = rep.setdefault(key, n)
@@ -364,8 +399,8 @@ def _launch(plan: KernelPlan, kern: Kernel, stores: list[_Storage], n: int,
 # skips _prepare/_bind — their outcome depends only on those shapes — and is
 # a single C call (SURVEY.md 7.3 "host overhead per call").
 
-_FAST: dict = {}
-_FAST_NAMES: dict = {}
+_FAST = _LRU(512)
+_FAST_NAMES = _LRU(4096)
 
 
 def _program_names(vs) -> list[str]:
@@ -378,7 +413,7 @@ def _program_names(vs) -> list[str]:
         for nm in [v.stmt.lhs.field] + _rhs_names(v):
             if nm not in names:
                 names.append(nm)
-    _FAST_NAMES[key] = (tuple(vs), names)
+    _FAST_NAMES.put(key, (tuple(vs), names))
     return names
 
 
@@ -413,12 +448,10 @@ def _fast_run(key) -> bool:
 def _fast_record(key, vs, kern: Kernel, stores: list, n: int) -> None:
     if key is None or n == 0 or any(s.where != "cuda" or s.pitch < 0 for s in stores):
         return
-    if len(_FAST) > 512:
-        _FAST.clear()
     from .runtime import address_arrays
 
     bases, pitches = address_arrays([s.base for s in stores], [s.pitch for s in stores])
-    _FAST[key] = (tuple(vs), kern, n, bases, pitches, stores[0].device.index)
+    _FAST.put(key, (tuple(vs), kern, n, bases, pitches, stores[0].device.index))
 
 
 # -------------------------------------------------------------- public API --
@@ -482,50 +515,117 @@ def eval_statement_per_component(v, env: Env) -> None:
         _launch(plan, kern, stores, n)
 
 
+def _fusion_plan(vs, env: Env):
+    """Whether a program can run as ONE fused launch with the reference's
+    sequential semantics, decided WITHOUT touching any field: ``(n,
+    resizes)`` — the common gridsize and the ``=`` targets to resize first —
+    or None when it must run statement by statement.
+
+    The reference prepares each statement just before running it
+    (evaluator.py:180-201 per call, cli.py:97-99 in order): a ``=`` target
+    is resized (zero-filled) only when its turn comes, after the earlier
+    statements have read it.  Hoisting that resize in front of the fused
+    launch is exact only if no earlier statement touched the field, so the
+    gridsizes are simulated here statement by statement; any statement that
+    would fail (missing field, disagreeing sizes, ``op=`` needing a resize),
+    a resize of a field an earlier statement used, or mixed gridsizes send
+    the program down the sequential path, which raises — or resizes — at
+    exactly the reference's point."""
+    sim: dict[str, int] = {}
+    touched: set[str] = set()
+    resizes = []
+    n_all = None
+    for v in vs:
+        name = v.stmt.lhs.field
+        lhs = env.get(name) if hasattr(env, "get") else None
+        if lhs is None or not _is_tensor_field(lhs):
+            return None
+        sizes = []
+        for nm in _rhs_names(v):
+            f = env.get(nm)
+            if f is None or not hasattr(f, "gridsize"):
+                return None
+            sizes.append(sim.get(nm, f.gridsize))
+        if len(set(sizes)) > 1:
+            return None
+        cur = sim.get(name, lhs.gridsize)
+        n = sizes[0] if sizes else cur
+        if sizes and n == 0:
+            return None
+        if cur != n:
+            if v.stmt.op != "=" or name in touched:
+                return None
+            resizes.append((lhs, n))
+            sim[name] = n
+        touched.add(name)
+        touched.update(_rhs_names(v))
+        if n_all is None:
+            n_all = n
+        elif n != n_all:
+            return None
+    return n_all, resizes
+
+
+def _sequential(vs, env: Env) -> None:
+    for v in vs:
+        eval_statement(v, env)
+
+
 @_nvtx
 def eval_program(vs: Sequence[Any], env: Env) -> None:
     """Execute statements in order, fused into ONE kernel when they share a
     gridsize (else one launch per statement).  Bitwise identical to
-    ``for v in vs: eval_statement(v, env)`` (S11)."""
+    ``for v in vs: eval_statement(v, env)`` (S11), errors included: a
+    statement that fails does so after the statements before it ran."""
     vs = list(vs)
     if not vs:
         return
     key = _fast_key(vs, env)
     if key is not None and _fast_run(key):
         return
-    sizes = []
-    for k, v in enumerate(vs):
-        try:
-            sizes.append(_prepare(v, env)[1])
-        except EvalError:
-            if k:
-                eval_program(vs[:k], env)  # the reference ran those before failing
+    fp = _fusion_plan(vs, env)
+    if fp is None:
+        _sequential(vs, env)
+        return
+    n, resizes = fp
+    try:
+        # lowering folds literal-only subtrees with the reference's Python
+        # scalar semantics and may raise (ZeroDivisionError on `1/0`) — the
+        # reference raises it only when that statement's turn comes
+        binding = _bind(vs, env)
+    except ArithmeticError:
+        if len(vs) == 1:
             raise
-    if len(set(sizes)) == 1 and all(_lookup(env, nm).gridsize == sizes[0]
-                                    for v in vs for nm in [v.stmt.lhs.field] + _rhs_names(v)):
-        plan, kern, stores = _bind(vs, env)
-        _launch(plan, kern, stores, sizes[0])
-        _fast_record(_fast_key(vs, env), vs, kern, stores, sizes[0])
-    else:
-        for v in vs:
-            eval_statement(v, env)
+        _sequential(vs, env)
+        return
+    for lhs, size in resizes:
+        lhs.resize(size)
+    if resizes:
+        binding = _bind(vs, env)
+    plan, kern, stores = binding
+    _launch(plan, kern, stores, n)
+    _fast_record(_fast_key(vs, env), vs, kern, stores, n)
 
 
 class _BatchCache:
-    def __init__(self) -> None:
-        self._d: dict = {}
+    """Uploaded domain tables by (kernel, table contents), LRU-bounded.  An
+    evicted Batch frees its device table when the last reference goes, so
+    anything that launches it later — a ``Bound`` from ``bind_batch``, a
+    graph from ``capture_graph`` — holds its own reference."""
+
+    def __init__(self, cap: int = 64) -> None:
+        self._d = _LRU(cap)
 
     def get(self, kern: Kernel, table: tuple, stream: int) -> Batch:
         key = (id(kern), table)
-        b = self._d.get(key)
-        if b is None:
-            bases = [[t[0] for t in dom[1]] for dom in table]
-            pitches = [[t[1] for t in dom[1]] for dom in table]
-            ns = [dom[0] for dom in table]
-            b = Batch(kern, bases, pitches, ns, stream)
-            if len(self._d) > 64:
-                self._d.clear()
-            self._d[key] = b
+        hit = self._d.get(key)
+        if hit is not None and hit[0] is kern:
+            return hit[1]
+        bases = [[t[0] for t in dom[1]] for dom in table]
+        pitches = [[t[1] for t in dom[1]] for dom in table]
+        ns = [dom[0] for dom in table]
+        b = Batch(kern, bases, pitches, ns, stream)
+        self._d.put(key, (kern, b))
         return b
 
 
@@ -534,9 +634,9 @@ _batches = _BatchCache()
 
 # eval_batch steady state: the same environments, whose fields are the same
 # (live) tensor objects as at the previous call, reuse that call's uploaded
-# table — an identity check per field instead of re-validating and
+# tables — an identity check per field instead of re-validating and
 # re-binding every subdomain (24 ms of host time for C4's 512 domains).
-_BATCH_FAST: dict = {}
+_BATCH_FAST = _LRU(64)
 
 
 def _batch_tensors(vs, envs):
@@ -565,29 +665,60 @@ def _device_groups(vs, envs) -> dict:
     return groups
 
 
+def _cross_domain_hazard(spans: list) -> bool:
+    """``spans``: (start, end, domain, writes) byte ranges of every field of
+    every subdomain.  True when a range some subdomain WRITES overlaps any
+    range of another subdomain (a read-after-write, write-after-read or
+    write-write race once all subdomains run concurrently in one launch).
+    Within one subdomain distinct fields never overlap (_check_disjoint), so
+    a connected group of overlapping ranges that holds a write and more than
+    one subdomain always contains such a pair."""
+    spans.sort()
+    end = -1
+    doms: set = set()
+    wr = False
+    for lo, hi, d, w in spans:
+        if lo >= end:  # a new connected group
+            if wr and len(doms) > 1:
+                return True
+            end, doms, wr = hi, {d}, w
+        else:
+            end = max(end, hi)
+            doms.add(d)
+            wr = wr or w
+    return wr and len(doms) > 1
+
+
 def _batch_plan(vs, envs):
     """(kernel, table key, device) of a batchable program over `envs`, or
-    None when it must run as sequential launches."""
+    None when it must run as sequential launches: a subdomain that cannot
+    fuse (see _fusion_plan), host fields, or storage shared between
+    subdomains where one of them writes (reads of another
+    subdomain's outputs, partially overlapping halo views)."""
     table = []
-    plan = kern = None
-    written: set = set()
-    shared_write = False
-    for env in envs:
-        sizes = {_prepare(v, env)[1] for v in vs}
+    spans = []
+    plan = kern = written = None
+    for d, env in enumerate(envs):
+        fp = _fusion_plan(vs, env)
+        if fp is None:
+            return None
+        n, resizes = fp
+        for lhs, size in resizes:  # hoistable by construction (_fusion_plan)
+            lhs.resize(size)
         p, k, stores = _bind(vs, env)
         if kern is None:
             plan, kern = p, k
-            wf = {fi for fi, fl in zip(plan.slot_field, plan.slot_flags)
-                  if fl & lowering.SLOT_WRITE}
+            written = {fi for fi, fl in zip(plan.slot_field, plan.slot_flags)
+                       if fl & lowering.SLOT_WRITE}
         elif k is not kern:
             raise EvalError("subdomains of one batch must share field shapes and aliasing")
-        if len(sizes) != 1 or any(s.where != "cuda" or s.pitch < 0 for s in stores):
+        if any(s.where != "cuda" or s.pitch < 0 for s in stores):
             return None
-        for fi in wf:  # a field written by two subdomains would race
-            shared_write |= stores[fi].key in written
-            written.add(stores[fi].key)
-        table.append((sizes.pop(), tuple((s.base, s.pitch) for s in stores), stores[0].device))
-    if shared_write or len({t[2] for t in table}) > 1:
+        for fi, s in enumerate(stores):
+            if s.extent:
+                spans.append((s.base, s.base + 8 * s.extent, d, fi in written))
+        table.append((n, tuple((s.base, s.pitch) for s in stores), stores[0].device))
+    if len({t[2] for t in table}) > 1 or _cross_domain_hazard(spans):
         return None
     return kern, tuple((t[0], t[1]) for t in table), table[0][2]
 
@@ -603,8 +734,10 @@ def _batch_launch(kern, key, dev) -> None:
 @_nvtx
 def eval_batch(vs, envs: Sequence[Env]) -> None:
     """Execute a statement (or a program) over many independent subdomains
-    in ONE launch.  ``envs[d]`` is subdomain d's data environment; the result
-    is bitwise identical to ``for env in envs: eval_program(vs, env)``."""
+    in ONE launch per GPU.  ``envs[d]`` is subdomain d's data environment;
+    the result is bitwise identical to ``for env in envs: eval_program(vs,
+    env)`` — subdomains that share written storage, or that cannot fuse,
+    run exactly that way instead."""
     if not isinstance(vs, (list, tuple)):
         vs = [vs]
     if not envs:
@@ -615,30 +748,30 @@ def eval_batch(vs, envs: Sequence[Env]) -> None:
         cur = _batch_tensors(vs, envs)
         if cur is not None and len(cur) == len(hit[1]) and all(
                 a is r() for a, r in zip(cur, hit[1])):
-            _batch_launch(*hit[2])
+            for bp in hit[2]:
+                _batch_launch(*bp)
             return
-    groups = _device_groups(vs, envs)
-    if len(groups) > 1:
-        # subdomains spread over several GPUs of this process: one batched
-        # launch per GPU (asynchronous, so the GPUs run concurrently)
-        for idx in groups.values():
-            eval_batch(vs, [envs[i] for i in idx])
-        return
-    bp = _batch_plan(vs, envs)
-    if bp is None:
-        for env in envs:  # not batchable: sequential launches, same bits
-            eval_program(vs, env)
-        return
-    _batch_launch(*bp)
-    tensors = _batch_tensors(vs, envs)
+    # subdomains spread over several GPUs of this process: one batched
+    # launch per GPU (asynchronous, so the GPUs run concurrently)
+    bps = []
+    for idx in _device_groups(vs, envs).values():
+        sub = envs if len(idx) == len(envs) else [envs[i] for i in idx]
+        bp = _batch_plan(vs, sub)
+        if bp is None:
+            for env in sub:  # not batchable: sequential launches, same bits
+                eval_program(vs, env)
+            bps = None
+            continue
+        _batch_launch(*bp)
+        if bps is not None:
+            bps.append(bp)
+    tensors = _batch_tensors(vs, envs) if bps else None
     if tensors is not None:
         import weakref
 
-        if len(_BATCH_FAST) > 64:
-            _BATCH_FAST.clear()
         # weak references: the cache never keeps fields alive, and a freed
         # tensor can never match (its reference is dead)
-        _BATCH_FAST[fkey] = (len(envs), [weakref.ref(t) for t in tensors], bp, tuple(vs))
+        _BATCH_FAST.put(fkey, (len(envs), [weakref.ref(t) for t in tensors], bps, tuple(vs)))
 
 
 class Bound:
@@ -646,11 +779,13 @@ class Bound:
     kernel once (one C call, no validation) on the current stream of the
     fields' device — the host-side analogue of a CUDA graph.  Valid while no
     bound field is resized or reallocated; results are bitwise those of
-    ``eval_program`` / ``eval_batch``."""
+    ``eval_program`` / ``eval_batch``.  Holds the kernel (and batch table)
+    it launches."""
 
-    def __init__(self, fn, kernel: Kernel):
+    def __init__(self, fn, kernel: Kernel, batch: Batch | None = None):
         self._fn = fn
         self.kernel = kernel
+        self.batch = batch
 
     def __call__(self) -> None:
         self._fn()
@@ -663,11 +798,17 @@ def bind_program(vs, env: Env) -> Bound:
     if not isinstance(vs, (list, tuple)):
         vs = [vs]
     vs = list(vs)
-    sizes = {_prepare(v, env)[1] for v in vs}
-    if len(sizes) != 1:
-        raise EvalError("bind_program needs one gridsize for the whole program")
-    n = sizes.pop()
-    plan, kern, stores = _bind(vs, env)
+    fp = _fusion_plan(vs, env)
+    if fp is None:
+        raise EvalError("bind_program needs a program that runs as one fused launch: one "
+                        "gridsize, every field present, and no statement resizing a field "
+                        "an earlier statement uses")
+    n, resizes = fp
+    plan, kern, stores = _bind(vs, env)  # lowering errors surface before any resize
+    for lhs, size in resizes:
+        lhs.resize(size)
+    if resizes:
+        plan, kern, stores = _bind(vs, env)
     if any(s.where != "cuda" or s.pitch < 0 for s in stores) or \
             len({s.device for s in stores}) != 1:
         raise EvalError("bind_program needs device fields on one GPU with uniform pitches")
@@ -692,27 +833,39 @@ def bind_batch(vs, envs: Sequence[Env]) -> Bound:
     bp = _batch_plan(list(vs), envs)
     if bp is None:
         raise EvalError("these subdomains cannot share one launch (mixed sizes, host fields, "
-                        "several GPUs, or a field written by two subdomains)")
+                        "several GPUs, or storage one subdomain writes and another uses)")
     kern, key, dev = bp
     import torch
 
     with torch.cuda.device(dev):
-        _batches.get(kern, key, torch.cuda.current_stream(dev).cuda_stream)
-    return Bound(lambda: _batch_launch(kern, key, dev), kern)
+        batch = _batches.get(kern, key, torch.cuda.current_stream(dev).cuda_stream)
+
+    def go():
+        with torch.cuda.device(dev):
+            batch.launch(torch.cuda.current_stream(dev).cuda_stream)
+
+    return Bound(go, kern, batch)
 
 
 def capture_graph(fn, warmup: int = 1):
     """Run ``fn`` ``warmup`` times (compiles kernels, uploads batch tables),
     then capture one call into a CUDA graph; returns the graph — ``.replay()``
-    re-executes every launch of ``fn`` with one host call."""
+    re-executes every launch of ``fn`` with one host call.  The graph holds
+    a reference to every kernel and batch table it launches
+    (``graph.tlb_pins``), so cache eviction can never free what a replay
+    still addresses."""
     import torch
+
+    from .runtime import pin_scope
 
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        fn()
+    with pin_scope() as pins:
+        with torch.cuda.graph(g):
+            fn()
+    g.tlb_pins = pins
     return g
 
 

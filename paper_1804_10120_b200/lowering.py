@@ -138,7 +138,7 @@ class _Lit:
         if math.isfinite(x):
             return f"({x.hex()})"
         bits = struct.unpack("<q", struct.pack("<d", x))[0]
-        return f"__longlong_as_double({bits}LL)"
+        return f"(__longlong_as_double({bits}LL))"
 
 
 @dataclass
@@ -220,6 +220,13 @@ class _Builder:
     def write(self, f: int, c: int, val) -> None:
         s = self.slot(f, c)
         self.slot_flags[s] |= SLOT_WRITE
+        if isinstance(val, _Lit):
+            # a literal stored into a field becomes a float64 array element in
+            # the reference (evaluator.py:150-161); later reads of it take part
+            # in numpy array arithmetic under errstate(divide/invalid="ignore")
+            # (evaluator.py:224) — IEEE inf/nan, never a Python
+            # ZeroDivisionError — so the shadow keeps np.float64 semantics
+            val = _Lit(np.float64(val.value))
         self.shadow[s] = val
         self.instrs.append(Instr("st", a=val, slot=s))
 
@@ -468,6 +475,7 @@ class Variant:
     threads: int = 256  # TLK_THREADS: block size of the flat and batch entries
     stage_threads: int = 128  # TLK_STAGE_THREADS: the staged entry's block = tile (points)
     stage_reads: int = 0  # read slots copied through the ring (0 = all; the rest load directly)
+    minb: int = 0  # TLK_MINB: min resident blocks/SM of the flat entries (0 = unconstrained)
 
     def tag(self) -> str:
         t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
@@ -476,6 +484,7 @@ class Variant:
         t += f"k{self.batch_threads}" if self.batch_threads else ""
         t += f"g{self.stage}x{self.stage_threads}" if self.stage else ""
         t += f"r{self.stage_reads}" if self.stage and self.stage_reads else ""
+        t += f"m{self.minb}" if self.minb else ""
         return t + (f"n{self.threads}" if self.threads != 256 else "")
 
     def small_class(self) -> "Variant":
@@ -499,9 +508,9 @@ class Variant:
         """Whether two variants compile to the same cubin (vec/waves are
         launch-time choices; both entry points are in every module)."""
         return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs, self.stage,
-                 self.threads, self.stage_threads, self.stage_reads)
+                 self.threads, self.stage_threads, self.stage_reads, self.minb)
                 == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs, other.stage,
-                    other.threads, other.stage_threads, other.stage_reads))
+                    other.threads, other.stage_threads, other.stage_reads, other.minb))
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -614,6 +623,8 @@ def _env_variant(v: Variant) -> Variant:
         kw["stage_threads"] = int(env["TLK_STAGE_THREADS"])
     if "TLK_STAGE_READS" in env:
         kw["stage_reads"] = int(env["TLK_STAGE_READS"])
+    if "TLK_MINB" in env:
+        kw["minb"] = int(env["TLK_MINB"])
     if kw:
         kw["small_n"] = 0  # a forced variant applies at every size ...
     if "TLK_SMALL_N" in env:
@@ -707,6 +718,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         header.append("// " + _statement_comment(v))
     header.append(f"#define TLK_NSLOTS {n_slots}")
     header.append(f"#define TLK_THREADS {variant.threads}")
+    if variant.minb:
+        header.append(f"#define TLK_MINB {variant.minb}")
     if variant.stage:
         header.append(f"#define TLK_NSTAGE {variant.stage}")
         header.append(f"#define TLK_NREAD {len(rord) - rord.count(-1)}")

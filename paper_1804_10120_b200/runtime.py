@@ -7,10 +7,12 @@ or NVRTC or the GPU is missing, the calls below raise ``TlbError``.
 
 from __future__ import annotations
 
+import atexit
 import ctypes
 import hashlib
 import os
 import threading
+from collections import OrderedDict
 from pathlib import Path
 from typing import Sequence
 
@@ -47,6 +49,17 @@ class TlbError(RuntimeError):
 
 _lib = None
 _lib_lock = threading.Lock()
+_exiting = False
+
+
+def _at_exit() -> None:
+    # the CUDA context may already be gone at interpreter shutdown: modules
+    # are released with the process there, not one by one
+    global _exiting
+    _exiting = True
+
+
+atexit.register(_at_exit)
 
 c_ll = ctypes.c_longlong
 c_vp = ctypes.c_void_p
@@ -135,6 +148,35 @@ def _arr(ctype, values):
     return (ctype * len(values))(*values)
 
 
+# ------------------------------------------------------- graph capture pins
+# A CUDA graph bakes in kernel handles and batch-table addresses.  While a
+# pin scope is open on this thread (evaluator.capture_graph), every Kernel
+# and Batch that launches is recorded, and the graph keeps that list, so
+# neither the module nor the table can be freed under a later replay.
+
+_pins = threading.local()
+
+
+class pin_scope:
+    def __enter__(self) -> list:
+        self.prev = getattr(_pins, "cur", None)
+        _pins.cur = []
+        return _pins.cur
+
+    def __exit__(self, *exc) -> None:
+        _pins.cur = self.prev
+
+
+_launch_count = [0]
+
+
+def _pin(obj) -> None:
+    _launch_count[0] += 1
+    cur = getattr(_pins, "cur", None)
+    if cur is not None:
+        cur.append(obj)
+
+
 class Kernel:
     """A compiled fused kernel (cubin + slot map); modules load per context."""
 
@@ -220,6 +262,7 @@ class Kernel:
         check(lib().tlb_launch(handle, n, _arr(c_vp, bases), _arr(c_ll, pitches), vec,
                                threads, max_blocks, stream), "tlb_launch")
         self.launches += 1
+        _pin(self)
 
     def launch_arrays(self, n: int, bases, pitches, stream: int) -> None:
         """Launch with prebuilt ctypes address arrays (bound-launch fast path)."""
@@ -232,6 +275,18 @@ class Kernel:
         if rc:
             check(rc, "tlb_launch")
         self.launches += 1
+        _pin(self)
+
+    def __del__(self):
+        # unloads the module from every context it was loaded into (after
+        # the context's pending work); evicted kernels only ever reach this
+        # once nothing — plan cache, bound launch, batch, graph — holds them
+        try:
+            if getattr(self, "handle", None) and _lib is not None and not _exiting:
+                _lib.tlb_kernel_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
 
     def exec_host(self, n: int, comp_ptrs: Sequence[Sequence[int]], stream: int,
                   slab: int = 0) -> None:
@@ -240,6 +295,7 @@ class Kernel:
             *[ctypes.cast(r, ctypes.POINTER(c_vp)) for r in rows])
         check(lib().tlb_exec_host(self.handle, n, outer, slab, stream), "tlb_exec_host")
         self.launches += 1
+        _pin(self)
 
 
 def address_arrays(bases: Sequence[int], pitches: Sequence[int]):
@@ -267,38 +323,49 @@ class Batch:
         check(lib().tlb_batch_launch(self.handle, self.kernel.batch_vec, threads, stream),
               "tlb_batch_launch")
         self.kernel.launches += 1
+        _pin(self)
 
     def __del__(self):
         try:
-            if self.handle and _lib is not None:
+            if self.handle and _lib is not None and not _exiting:
                 _lib.tlb_batch_destroy(self.handle)
         except Exception:
             pass
 
 
-_kernels: dict[str, Kernel] = {}
+KERNEL_CACHE_SIZE = 256
+_kernels: "OrderedDict[str, Kernel]" = OrderedDict()
 _kernels_lock = threading.Lock()
 
 
 def get_kernel(plan: KernelPlan) -> Kernel:
-    """Compiled kernel for `plan`, cached in memory by source (and on disk
-    by source + options + NVRTC version)."""
+    """Compiled kernel for `plan`, cached in memory by source (LRU, at most
+    KERNEL_CACHE_SIZE; on disk by source + options + NVRTC version)."""
     key = plan.key + "|" + " ".join(compile_options())
-    k = _kernels.get(key)
-    if k is None:
-        with _kernels_lock:
-            k = _kernels.get(key)
-            if k is None:
-                k = Kernel(plan)
-                if plan.small_variant is not None:
-                    small = Kernel(plan.small_plan) if plan.small_plan is not None else None
-                    k._attach_small(plan.variant.small_n, plan.small_variant, small)
-                _kernels[key] = k
+    with _kernels_lock:
+        k = _kernels.get(key)
+        if k is not None:
+            _kernels.move_to_end(key)
+            return k
+        k = Kernel(plan)
+        if plan.small_variant is not None:
+            small = Kernel(plan.small_plan) if plan.small_plan is not None else None
+            k._attach_small(plan.variant.small_n, plan.small_variant, small)
+        _kernels[key] = k
+        while len(_kernels) > KERNEL_CACHE_SIZE:
+            _kernels.popitem(last=False)
     return k
 
 
 def all_kernels() -> list[Kernel]:
-    return list(_kernels.values())
+    with _kernels_lock:
+        return list(_kernels.values())
+
+
+def total_launches() -> int:
+    """Fused-kernel launches (plain, staged, batched, host-staged) issued by
+    this process so far, whichever kernel objects are still cached."""
+    return _launch_count[0]
 
 
 def release_staging() -> None:

@@ -21,6 +21,24 @@ def case_names() -> list[str]:
     return sorted(manifest()["cases"])
 
 
+def run_case(case: dict, fn, exact: bool = True) -> None:
+    """Run ``fn`` (a whole golden program); when the reference stopped
+    part-way through (``case["raises"]``), expect that error — same type
+    name and message when ``exact`` (the product), any error otherwise (the
+    CPU oracle) — the targets are then compared as the reference left them."""
+    import pytest
+
+    want = case.get("raises")
+    if not want:
+        fn()
+        return
+    with pytest.raises(Exception) as ei:
+        fn()
+    if exact:
+        assert type(ei.value).__name__ == want["type"], ei.value
+        assert str(ei.value) == want["message"]
+
+
 def program(source: str):
     from paper_1804_10120_b200.ir import validate_statement
     from paper_1804_10120_b200.parser import parse_program

@@ -21,7 +21,14 @@ def _sass(kernel) -> str:
 
 @pytest.mark.parametrize("name", case_names())
 def test_every_golden_program_compiles_for_sm100a(name):
-    _, vs = program(manifest()["cases"][name]["source"])
+    case = manifest()["cases"][name]
+    _, vs = program(case["source"])
+    if case.get("raises", {}).get("type") == "ZeroDivisionError":
+        # a literal `1/0`: the reference raises when the statement runs, and
+        # so does lowering (Python-scalar folding); the statements before it lower
+        with pytest.raises(ZeroDivisionError):
+            lower_program(vs)
+        vs = vs[:-1]
     plan = lower_program(vs)
     k = get_kernel(plan)
     assert len(k.cubin()) > 0

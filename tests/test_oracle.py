@@ -5,7 +5,7 @@ golden case, the per-point restatement within tl_compare's 1e-13."""
 import numpy as np
 import pytest
 
-from helpers import case_names, golden_io, manifest, program, same_bits
+from helpers import case_names, golden_io, manifest, program, run_case, same_bits
 from oracle import numpy_eval, pointwise
 
 
@@ -14,7 +14,7 @@ def test_numpy_oracle_bitwise_equals_reference(name):
     case = manifest()["cases"][name]
     _, vs = program(case["source"])
     env, want = golden_io(name)
-    numpy_eval.eval_program(vs, env)
+    run_case(case, lambda: numpy_eval.eval_program(vs, env), exact=False)
     for t in case["targets"]:
         assert same_bits(env[t], want[t]), t
 
@@ -25,6 +25,8 @@ def test_pointwise_oracle_within_tolerance(name):
     case = manifest()["cases"][name]
     _, vs = program(case["source"])
     env, want = golden_io(name)
+    if case.get("raises") or case.get("sizes"):
+        pytest.skip("the per-point oracle has no gridsize/error semantics")
     for v in vs:
         pointwise.run(v, env)
     for t in case["targets"]:
