@@ -19,6 +19,13 @@ are git-ignored but travel to the GPU box with the repo snapshot.
      design: one thread per (point, LHS component), device pointer arrays),
      compiled as-is with nvcc for sm_100a into _ref/<program>_cuda.so — the
      comparator of SURVEY.md 8f #3 (driven by oracle/refcuda.py).
+  4. The reference package itself (pkg/src/tlang, unmodified) as a build
+     artefact under _ref/tlang, so that its numpy evaluator — the paper's
+     "NonAccel" CPU path (evaluator.py:204-236, chunk + ThreadPoolExecutor)
+     — can be timed on the GPU box's host cores beside the device numbers
+     (bench.py, oracle/refnumpy.py).  Like the .so files it is git-ignored
+     and travels with the repo snapshot; nothing under the product package
+     imports it.
 
 Usage: python oracle/build_ref.py [--force]
 """
@@ -69,6 +76,16 @@ def build(force: bool = False) -> Path:
         exe = OUT / name
         if force or not exe.exists():
             _run([cc, *flags, *map(str, srcs), "-o", str(exe), *libs])
+
+    pkg = OUT / "tlang"
+    src_pkg = REF / "src" / "tlang"
+    stamp = "".join(f"{p.name}:{p.stat().st_size}:{p.stat().st_mtime_ns};"
+                    for p in sorted(src_pkg.glob("*.py")))
+    if force or not (pkg / ".stamp").exists() or (pkg / ".stamp").read_text() != stamp:
+        if pkg.exists():
+            shutil.rmtree(pkg)
+        shutil.copytree(src_pkg, pkg, ignore=shutil.ignore_patterns("__pycache__"))
+        (pkg / ".stamp").write_text(stamp)
 
     sys.path.insert(0, str(REF / "src"))
     from tlang.ir import validate_statement

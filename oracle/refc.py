@@ -83,6 +83,49 @@ class RefProgram:
             if pool is not None:
                 pool.shutdown()
 
+    def slab_runner(self, env: dict, n: int, threads: int, min_slab: int = 1024):
+        """A callable running every entry over ``env`` split into per-thread
+        slabs (as ``run``), with all pointer tables bound once up front so
+        that repeated calls time only the kernels."""
+        slabs = _slabs(n, threads, min_slab)
+        calls = [[self._bind(self.by_ordinal[o], env, lo, hi) for lo, hi in slabs]
+                 for o in self.order]
+        pool = ThreadPoolExecutor(max_workers=len(slabs)) if len(slabs) > 1 else None
+
+        def go():
+            for per_entry in calls:
+                if pool is None:
+                    for c in per_entry:
+                        c()
+                else:
+                    list(pool.map(lambda c: c(), per_entry))
+
+        return go
+
+    def domain_runner(self, envs: list, threads: int):
+        """A callable running the program over many subdomains, one task per
+        subdomain (its entries in manifest order) on ``threads`` workers —
+        how a multi-domain CPU code parallelises (multi-domain
+        loops live outside TLoops)."""
+        tasks = []
+        for env in envs:
+            npts = next(iter(env.values())).shape[-1]
+            tasks.append([self._bind(self.by_ordinal[o], env, 0, npts) for o in self.order])
+        pool = ThreadPoolExecutor(max_workers=threads) if threads > 1 else None
+
+        def one(task):
+            for c in task:
+                c()
+
+        def go():
+            if pool is None:
+                for t in tasks:
+                    one(t)
+            else:
+                list(pool.map(one, tasks))
+
+        return go
+
     def _bind(self, entry: TlEntry, env: dict, lo: int, hi: int):
         tensors, scalars, numbers, keep = [], [], [], []
         for a in range(entry.n_args):

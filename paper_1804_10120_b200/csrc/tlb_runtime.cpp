@@ -414,7 +414,10 @@ int tlb_compile(const char* src, const char* const* opts, int nopts, const char*
     if (smem > 227 * 1024) return fail("tlb_compile: staged tile ring of %lld bytes", smem);
     k->stage_smem = (int)smem;
     const long long bsmem = smem + nstage * source_define(src, "TLK_NSLOTS", 0) * 8;
-    k->stage_batch_smem = bsmem <= 227 * 1024 ? (int)bsmem : 0;  // 0: no staged batch
+    // the staged batch entry is compiled only into modules that ask for it
+    // (TLK_STAGE_BATCH, lowering Variant.batch_vec = 3); 0: no staged batch
+    k->stage_batch_smem =
+        source_define(src, "TLK_STAGE_BATCH", 0) && bsmem <= 227 * 1024 ? (int)bsmem : 0;
   }
   if (file_exists(cache_path) && read_file(cache_path, &k->cubin)) {
     *out = k.release();

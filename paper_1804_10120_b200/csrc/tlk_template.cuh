@@ -375,6 +375,7 @@ tlk_stage_v1(const tlk_flat_params prm) {
 // slot from global memory.  Consumers release a stage through empty[s]; the
 // producer refills it NSTAGE items later.  Pointer block: NSTAGE x NSLOTS
 // pointers after the ring.
+#ifdef TLK_STAGE_BATCH  // opt-in (Variant.batch_vec = 3): measured slower than tlk_batch_v1
 __device__ __forceinline__ void tlk_mbar_wait(unsigned b, unsigned phase) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -481,4 +482,5 @@ tlk_stage_batch_v1(const long long* __restrict__ table, const longlong2* __restr
     }
   }
 }
+#endif  // TLK_STAGE_BATCH
 #endif

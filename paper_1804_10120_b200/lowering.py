@@ -725,6 +725,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         header.append(f"#define TLK_NREAD {len(rord) - rord.count(-1)}")
         header.append(f"#define TLK_STAGE_THREADS {variant.stage_threads}")
         header.append("#define TLK_RORD {" + ",".join(map(str, rord)) + "}")
+        if variant.batch_vec == 3:
+            header.append("#define TLK_STAGE_BATCH 1")
     header.append(f"#define TLK_LDMODE {variant.ldmode}")
     header.append(f"#define TLK_BATCH_PTRS {variant.batch_ptrs}")
     src = "\n".join(header) + "\n" + template_text().replace("// @@TLK_BODY@@", body)

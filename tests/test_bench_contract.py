@@ -23,12 +23,39 @@ def _run(args, timeout=600):
 
 
 def test_reference_arm_line():
-    d = _run(["--impl", "reference", "--steps", "2", "--warmup", "1", "--cpu-sample", "4096"])
+    # every step covers ALL points of the workload (streamed in slabs), so
+    # the reference arm's config is our arm's config
+    d = _run(["--impl", "reference", "--steps", "2", "--warmup", "1", "--cpu-sample", "4096",
+              "--points", str(3 * 4096 + 1000)])
     assert REQUIRED <= set(d)
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
-    assert isinstance(d["config"], dict) and "workload" in d["config"]
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    assert d["config"] == bench.workload_config(3 * 4096 + 1000, 1)
+    assert "3 slabs of 4096 points (+1000)" in d["cpu_baseline"]["sample"]
+
+
+def test_config_table_is_compact_and_last():
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    gpu = {"rows": {"C1_dtg_64^3": {"N": 64**3, "us": 8.1, "frac": 0.87, "pts": 3.2e10}},
+           "floor_us": 2.0, "method": "m"}
+    cpu = {"C1_dtg_64^3": {"c": 2.7e8, "c_n": 64**3, "np1": 2.2e7, "np_n": 64**3, "npT": 1e7},
+           "host": "16x cpu"}
+    line = {"roofline": {"frac": 1.0}, "ms_per_step": 20.5, "value": 1.3e10,
+            "cpu_baseline": {"value": 8.5e7}}
+
+    class A:
+        points = 1 << 28
+
+    t = bench.config_table(gpu, cpu, line, A)
+    assert t["C1_dtg_64^3"] == [262144, 8.1, 0.87, 32000.0, 270.0, 22.0, 10.0]
+    assert t["C5_p2_2^28"][:2] == [1 << 28, 20500.0] and t["cpu_host"] == "16x cpu"
+    assert len(json.dumps(t)) < 2500
 
 
 @pytest.mark.gpu

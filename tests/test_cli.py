@@ -54,7 +54,10 @@ def test_check_matches_reference_cli(tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["c4_p3", "c2_maxwell", "seq_augmented"])
+@pytest.mark.parametrize("case", ["c4_p3", "c2_maxwell", "seq_augmented",
+                                  "fused_literal_div_zero", "augmented_div_after_literal",
+                                  "mixed_gridsize_read_before_resize",
+                                  "mixed_gridsize_resize_first_use"])
 @pytest.mark.parametrize("per_component", [False, True])
 def test_eval_writes_the_reference_container(case, per_component, tmp_path):
     from paper_1804_10120_b200 import tldf
@@ -72,3 +75,18 @@ def test_eval_writes_the_reference_container(case, per_component, tmp_path):
     for name, fld in tldf.read(GOLDEN / f"{case}.out.tldf", device="cpu").items():
         env[name] = fld
     assert out.read_bytes() == tldf.dumps(env)
+
+
+@pytest.mark.gpu
+def test_eval_stops_where_the_reference_stops(tmp_path):
+    # reference cli.py:93-99: an EvalError part-way through the program is a
+    # diagnostic (exit 2, "<file>: <message>"), and no output is written
+    spec = manifest()["cases"]["error_after_first_statement"]
+    f = tmp_path / "p.tl"
+    f.write_text(spec["source"])
+    out = tmp_path / "out.tldf"
+    res = _cli("eval", str(f), "--data", str(GOLDEN / "error_after_first_statement.in.tldf"),
+               "--out", str(out))
+    assert res.returncode == 2
+    assert res.stderr == f"{f}: {spec['raises']['message']}\n"
+    assert not out.exists()
