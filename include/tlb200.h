@@ -162,7 +162,12 @@ typedef struct tlb_harness_kernel {
 } tlb_harness_kernel;
 
 /* Stage the harness's host arrays through the GPU and run the kernel
- * (compiling it on first use; cubins cached under $TLB_CACHE_DIR if set). */
+ * (compiling it on first use; cubins cached under $TLB_CACHE_DIR if set).
+ * The generated `call` wrappers exit the harness process with
+ * TLB_HARNESS_EXIT_GPU (after printing tlb_last_error() with the kernel's
+ * tl_NNNN name) when this fails: the reference `call` returns void, and the
+ * harness's own exit codes 2-6 (tl_harness.c:14-15) keep their meaning. */
+#define TLB_HARNESS_EXIT_GPU 7
 int tlb_harness_call(tlb_harness_kernel* hk, long n, double** const* tensors,
                      const double* const* scalars);
 

@@ -53,14 +53,18 @@ def available(program: str) -> bool:
 class RefProgram:
     """One compiled reference program (all its statements, manifest order)."""
 
-    def __init__(self, program: str):
-        so = REF_DIR / f"{program}.so"
+    def __init__(self, program: str, so_path=None, manifest_path=None):
+        """``program``'s compiled reference C (oracle/_ref/<program>.so), or
+        any .so exporting the same bindings table (``so_path`` +
+        ``manifest_path``, e.g. the b200 bindings of registry.build_shared)."""
+        so = Path(so_path) if so_path else REF_DIR / f"{program}.so"
         if not so.exists():
             raise FileNotFoundError(f"{so} missing: run python oracle/build_ref.py")
         self.lib = ctypes.CDLL(str(so))
         count = c_int.in_dll(self.lib, "tloops_entry_count").value
         self.entries = (TlEntry * count).in_dll(self.lib, "tloops_entries")
-        manifest = (REF_DIR / f"{program}.manifest.tsv").read_text().splitlines()
+        man = Path(manifest_path) if manifest_path else REF_DIR / f"{program}.manifest.tsv"
+        manifest = man.read_text().splitlines()
         self.order = [int(line.split("\t")[0]) for line in manifest if line.strip()]
         self.by_ordinal = {e.ordinal: e for e in self.entries}
 

@@ -14,6 +14,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
@@ -79,6 +80,9 @@ struct Driver {
   CUresult (*MemcpyHtoD)(CUdeviceptr, const void*, size_t) = nullptr;
   CUresult (*MemcpyHtoDAsync)(CUdeviceptr, const void*, size_t, CUstream) = nullptr;
   CUresult (*MemcpyDtoHAsync)(void*, CUdeviceptr, size_t, CUstream) = nullptr;
+  CUresult (*MemHostRegister)(void*, size_t, unsigned) = nullptr;
+  CUresult (*MemHostUnregister)(void*) = nullptr;
+  CUresult (*PointerGetAttribute)(void*, CUpointer_attribute, CUdeviceptr) = nullptr;
 };
 
 // NVRTC subset (the nvrtcProgram handle is an opaque pointer).
@@ -164,7 +168,10 @@ int load_driver_locked() {
             bind(h, g_cu.MemAlloc, "cuMemAlloc_v2") && bind(h, g_cu.MemFree, "cuMemFree_v2") &&
             bind(h, g_cu.MemcpyHtoD, "cuMemcpyHtoD_v2") &&
             bind(h, g_cu.MemcpyHtoDAsync, "cuMemcpyHtoDAsync_v2") &&
-            bind(h, g_cu.MemcpyDtoHAsync, "cuMemcpyDtoHAsync_v2");
+            bind(h, g_cu.MemcpyDtoHAsync, "cuMemcpyDtoHAsync_v2") &&
+            bind(h, g_cu.MemHostRegister, "cuMemHostRegister_v2") &&
+            bind(h, g_cu.MemHostUnregister, "cuMemHostUnregister") &&
+            bind(h, g_cu.PointerGetAttribute, "cuPointerGetAttribute");
   if (!ok) return fail("tlb: libcuda.so.1 lacks a required symbol");
   CUresult r = g_cu.Init(0);
   if (r != CUDA_SUCCESS) return fail("tlb: cuInit failed (%d)", (int)r);
@@ -214,14 +221,27 @@ int bind_context(void* stream, CUcontext* out) {
 // --------------------------------------------------- per-context state ----
 
 constexpr int kStageBuffers = 3;  // host-staged pipeline depth (buffers = streams)
+constexpr int kMaxStageSets = 2;  // concurrent host-staged runs per context
 
-struct CtxState {
-  int sm_count = 0;
+// One host-staged pipeline's device buffers and streams.  A tlb_exec_host
+// call owns a set from acquisition until its final stream synchronisation;
+// the context's lock is held only to pick or return a set, so launches and
+// other staged runs (on this or any other context) never wait on a
+// synchronisation they are not part of.
+struct StageSet {
   CUstream side[kStageBuffers] = {};
   CUdeviceptr scratch = 0;
   size_t scratch_bytes = 0;
+  bool busy = false;
 };
-std::mutex g_ctx_mu;
+
+struct CtxState {
+  int sm_count = 0;
+  std::mutex stage_mu;
+  std::condition_variable stage_cv;
+  std::vector<std::unique_ptr<StageSet>> sets;
+};
+std::mutex g_ctx_mu;  // the map only (lookups and first-use initialisation)
 std::map<CUcontext, CtxState> g_ctx;
 
 int ctx_state(CUcontext ctx, CtxState** out) {
@@ -235,6 +255,73 @@ int ctx_state(CUcontext ctx, CtxState** out) {
   }
   *out = &st;
   return 0;
+}
+
+StageSet* acquire_stage_set(CtxState* st) {
+  std::unique_lock<std::mutex> lk(st->stage_mu);
+  for (;;) {
+    for (auto& s : st->sets)
+      if (!s->busy) {
+        s->busy = true;
+        return s.get();
+      }
+    if ((int)st->sets.size() < kMaxStageSets) {
+      st->sets.emplace_back(new StageSet);
+      st->sets.back()->busy = true;
+      return st->sets.back().get();
+    }
+    st->stage_cv.wait(lk);
+  }
+}
+
+void release_stage_set(CtxState* st, StageSet* set) {
+  {
+    std::lock_guard<std::mutex> lk(st->stage_mu);
+    set->busy = false;
+  }
+  st->stage_cv.notify_one();
+}
+
+// Page-lock pageable host ranges for the duration of one staged run
+// (TLB_HOST_REGISTER=1), so the copies are DMA'd directly instead of
+// through the driver's internal bounce buffers.  Ranges already pinned
+// (cudaHostAlloc / torch pin_memory, or registered by the caller) are left
+// alone; failures fall back to pageable copies.
+struct HostPins {
+  std::vector<void*> regs;
+  ~HostPins() {
+    for (void* p : regs) g_cu.MemHostUnregister(p);
+  }
+};
+
+bool host_register_enabled() {
+  const char* e = getenv("TLB_HOST_REGISTER");  // read per call (cheap next to a staged run)
+  return e && atoi(e) != 0;
+}
+
+void pin_host_ranges(std::vector<std::pair<uintptr_t, uintptr_t>> spans, HostPins* pins) {
+  const uintptr_t page = (uintptr_t)sysconf(_SC_PAGESIZE);
+  for (auto& sp : spans) {
+    sp.first = sp.first / page * page;
+    sp.second = (sp.second + page - 1) / page * page;
+  }
+  std::sort(spans.begin(), spans.end());
+  std::vector<std::pair<uintptr_t, uintptr_t>> merged;
+  for (auto& sp : spans) {
+    if (!merged.empty() && sp.first <= merged.back().second)
+      merged.back().second = std::max(merged.back().second, sp.second);
+    else
+      merged.push_back(sp);
+  }
+  for (auto& m : merged) {
+    unsigned int mt = 0;
+    if (g_cu.PointerGetAttribute(&mt, CU_POINTER_ATTRIBUTE_MEMORY_TYPE, (CUdeviceptr)m.first) ==
+        CUDA_SUCCESS)
+      continue;  // already page-locked (or device memory)
+    void* p = (void*)m.first;
+    if (g_cu.MemHostRegister(p, m.second - m.first, CU_MEMHOSTREGISTER_PORTABLE) == CUDA_SUCCESS)
+      pins->regs.push_back(p);
+  }
 }
 
 // ---------------------------------------------------------------- kernel ----
@@ -730,30 +817,46 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
   }
   slab = std::min(slab, n);
   slab = (slab + 255) / 256 * 256;  // keeps every slot slice 2 KiB aligned
-  std::lock_guard<std::mutex> lk(g_ctx_mu);  // one staged run per process at a time
+  HostPins pins;
+  if (host_register_enabled()) {
+    std::vector<std::pair<uintptr_t, uintptr_t>> spans;
+    for (size_t j = 0; j < m; ++j) {
+      const uintptr_t a = (uintptr_t)(comp_ptrs[k->slot_field[j]][k->slot_comp[j]]);
+      spans.emplace_back(a, a + (uintptr_t)n * sizeof(double));
+    }
+    pin_host_ranges(std::move(spans), &pins);
+  }
+  StageSet* set = acquire_stage_set(st);
+  struct Release {
+    CtxState* st;
+    StageSet* set;
+    ~Release() { release_stage_set(st, set); }
+  } release{st, set};
   size_t need = (size_t)nb * m * (size_t)slab * sizeof(double);
-  if (st->scratch_bytes < need) {
-    if (st->scratch) g_cu.MemFree(st->scratch);
-    st->scratch = 0;
-    st->scratch_bytes = 0;
-    CU(g_cu.MemAlloc(&st->scratch, need), "cuMemAlloc(staging)");
-    st->scratch_bytes = need;
+  if (set->scratch_bytes < need) {
+    if (set->scratch) g_cu.MemFree(set->scratch);
+    set->scratch = 0;
+    set->scratch_bytes = 0;
+    CU(g_cu.MemAlloc(&set->scratch, need), "cuMemAlloc(staging)");
+    set->scratch_bytes = need;
   }
   for (int s = 0; s < nb; ++s)
-    if (!st->side[s]) CU(g_cu.StreamCreate(&st->side[s], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+    if (!set->side[s])
+      CU(g_cu.StreamCreate(&set->side[s], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
   // order after prior work of the caller's stream
   CUevent ev;
   CU(g_cu.EventCreate(&ev, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
   CU(g_cu.EventRecord(ev, (CUstream)stream), "cuEventRecord");
-  for (int s = 0; s < nb; ++s) CU(g_cu.StreamWaitEvent(st->side[s], ev, 0), "cuStreamWaitEvent");
+  for (int s = 0; s < nb; ++s)
+    CU(g_cu.StreamWaitEvent(set->side[s], ev, 0), "cuStreamWaitEvent");
   g_cu.EventDestroy(ev);
   std::vector<uint64_t> slots(m);
   long long slab_idx = 0;
   for (long long lo = 0; lo < n; lo += slab, ++slab_idx) {
     const long long cnt = std::min(slab, n - lo);
     const int b = (int)(slab_idx % nb);
-    CUstream s = st->side[b];
-    CUdeviceptr buf = st->scratch + (size_t)b * m * (size_t)slab * sizeof(double);
+    CUstream s = set->side[b];
+    CUdeviceptr buf = set->scratch + (size_t)b * m * (size_t)slab * sizeof(double);
     for (size_t j = 0; j < m; ++j) {
       slots[j] = buf + j * (size_t)slab * sizeof(double);
       if (k->slot_flags[j] & TLB_SLOT_READ) {
@@ -769,7 +872,8 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
       }
     }
   }
-  for (int s = 0; s < nb; ++s) CU(g_cu.StreamSynchronize(st->side[s]), "cuStreamSynchronize");
+  for (int s = 0; s < nb; ++s)
+    CU(g_cu.StreamSynchronize(set->side[s]), "cuStreamSynchronize");
   return 0;
 }
 
@@ -777,12 +881,19 @@ int tlb_release_staging(void) {
   if (!g_driver_ok) return 0;
   CUcontext ctx = nullptr;
   g_cu.CtxGetCurrent(&ctx);
-  std::lock_guard<std::mutex> lk(g_ctx_mu);
-  auto it = g_ctx.find(ctx);
-  if (it != g_ctx.end() && it->second.scratch) {
-    CU(g_cu.MemFree(it->second.scratch), "cuMemFree(staging)");
-    it->second.scratch = 0;
-    it->second.scratch_bytes = 0;
+  CtxState* st = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    auto it = g_ctx.find(ctx);
+    if (it == g_ctx.end()) return 0;
+    st = &it->second;
+  }
+  std::lock_guard<std::mutex> lk(st->stage_mu);
+  for (auto& set : st->sets) {
+    if (set->busy || !set->scratch) continue;  // a running pipeline keeps its buffers
+    CU(g_cu.MemFree(set->scratch), "cuMemFree(staging)");
+    set->scratch = 0;
+    set->scratch_bytes = 0;
   }
   return 0;
 }

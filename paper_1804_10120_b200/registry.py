@@ -300,8 +300,12 @@ def render_bindings(entries: list[RegistryEntry]) -> str:
             "{",
             "  (void)D; /* literals are folded into the fused kernel */",
             f"  if (tlb_harness_call(&tl_hk_{tag}, N, T, S) != 0) {{",
-            f'    fprintf(stderr, "tloops_b200 entry {e.ordinal}: %s\\n", tlb_last_error());',
-            "    abort();",
+            "    /* the reference `call` has no error channel (void): report and",
+            "       exit with TLB_HARNESS_EXIT_GPU, past the harness's own 2-6 */",
+            f'    fprintf(stderr, "tl_harness: GPU kernel tl_{tag} (ordinal {e.ordinal}) '
+            f'failed: %s\\n", tlb_last_error());',
+            "    fflush(stderr);",
+            "    exit(TLB_HARNESS_EXIT_GPU);",
             "  }",
             "}",
             "",

@@ -88,7 +88,9 @@ def run(name, text, n, shapes):
     bases = [b.data_ptr() for b in bufs]
     pitches = [n if info.n_components > 1 else 0 for info in base.fields]
     want = None
-    for sname, (var, launch_kw) in shapes.items():
+    for sname, spec in shapes.items():
+        var, launch_kw = spec[0], spec[1]
+        os.environ["TLK_DEFINES"] = spec[2] if len(spec) > 2 else ""
         plan = lower_program(vs, variant=var)
         kern = get_kernel(plan)
         fn = lambda: kern.launch(n, bases, pitches,  # noqa: E731
@@ -146,8 +148,21 @@ def main():
         "v2_minb4": (Variant(**{**light.__dict__, "minb": 4}), {"vec": 2, "max_blocks": -4}),
         "v2_ldnc": (Variant(**{**light.__dict__, "ldmode": 1}), {"vec": 2, "max_blocks": -4}),
         "staged_policy": (v, {}),
+        "v1_t128": (Variant(**{**light.__dict__, "threads": 128}), {"vec": 1, "max_blocks": -4}),
+        "v1_t64": (Variant(**{**light.__dict__, "threads": 64}), {"vec": 1, "max_blocks": -8}),
+        "v1_onewave": (light, {"vec": 1, "max_blocks": 0}),
+        "v1_t128_onewave": (Variant(**{**light.__dict__, "threads": 128}),
+                            {"vec": 1, "max_blocks": 0}),
+        "v1_unroll2_onewave": (light, {"vec": 1, "max_blocks": 0}, "-DTLK_UNROLL=2"),
+        "v1_ldnc_t128": (Variant(**{**light.__dict__, "ldmode": 1, "threads": 128}),
+                         {"vec": 1, "max_blocks": -4}),
     }
+    if os.environ.get("ONLY_C1_NEW"):
+        c1 = {k: c1[k] for k in ("cur_v1_w4", "v1_t128", "v1_t64", "v1_onewave",
+                                 "v1_t128_onewave", "v1_unroll2_onewave", "v1_ldnc_t128")}
     run("C1_dtg", tb.DTG, 64**3, c1)
+    if os.environ.get("ONLY_C1_NEW"):
+        return
     prog, vs = tb.load(tb.CHRISTOFFEL)
     v3 = lower_program(vs).variant
     c3 = {
