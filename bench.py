@@ -421,7 +421,7 @@ def run_n_sweep(dist: Dist) -> dict:
     import torch
 
     from paper_1804_10120_b200 import bench as tb
-    from paper_1804_10120_b200 import eval_batch, eval_program
+    from paper_1804_10120_b200 import bind_batch, bind_program
     from paper_1804_10120_b200.partition import domain_bounds
 
     def timed(fn, k):
@@ -453,19 +453,20 @@ def run_n_sweep(dist: Dist) -> dict:
         for total in totals:
             lo, hi = slab(total, dist.rank, dist.world)
             env = fields(prog, vs, hi - lo)
-            t = timed(lambda: eval_program(vs, env), 10 if total <= 1 << 24 else 5)
+            t = timed(bind_program(vs, env), 10 if total <= 1 << 24 else 5)
             out[f"{name}_{total}"] = [total, round(t * 1e6, 2), float(f"{total / t:.4g}")]
             del env
             torch.cuda.empty_cache()
     prog, vs = tb.load(tb.P2)
     d0, d1 = domain_bounds(512, dist.rank, dist.world)
     envs = [fields(prog, vs, 16**3) for _ in range(d0, d1)]
-    t = timed(lambda: eval_batch(vs, envs), 10)
+    t = timed(bind_batch(vs, envs), 10)
     out["c4_p2_512x16^3"] = [512 * 16**3, round(t * 1e6, 2), float(f"{512 * 16**3 / t:.4g}")]
     del envs
     torch.cuda.empty_cache()
-    out["method"] = ("per-rank slabs (C4: whole subdomains per rank, one batched launch); 3 "
-                     "warm-up + 5-10 eager back-to-back launches, CUDA events, max over ranks")
+    out["method"] = ("per-rank slabs (C4: whole subdomains per rank, one batched launch); "
+                     "bound launches (bind_program / bind_batch: one C call each), 3 warm-up + "
+                     "5-10 eager back-to-back launches, CUDA events, max over ranks")
     return out
 
 
@@ -796,7 +797,7 @@ def run_configs() -> dict:
     import torch
 
     from paper_1804_10120_b200 import bench as tb
-    from paper_1804_10120_b200 import eval_batch, eval_program
+    from paper_1804_10120_b200 import bind_batch, bind_program
     from paper_1804_10120_b200.evaluator import plan_for
 
     peak, _ = measured_peak()
@@ -833,7 +834,7 @@ def run_configs() -> dict:
                          ("C2_maxwell_1e8", tb.MAXWELL, 10**8),
                          ("C3_christoffel_128^3", tb.CHRISTOFFEL, 128**3)):
         vs, env = fields(text, n)
-        record(key, n, timed(lambda: eval_program(vs, env)), plan_for(vs, env))
+        record(key, n, timed(bind_program(vs, env)), plan_for(vs, env))
         del env
         torch.cuda.empty_cache()
     for key, text in (("C4_p2_512x16^3", tb.P2), ("C4_p3_chain_512x16^3", tb.P3)):
@@ -842,16 +843,18 @@ def run_configs() -> dict:
         for d in range(512):
             vs, env = fields(text, 16**3, SEED + d)
             envs.append(env)
-        record(key, 512 * 16**3, timed(lambda: eval_batch(vs, envs)), plan_for(vs, envs[0]))
+        record(key, 512 * 16**3, timed(bind_batch(vs, envs)), plan_for(vs, envs[0]))
         del envs
         torch.cuda.empty_cache()
     tiny = torch.zeros(1, device="cuda")
     floor = single_cold(lambda: tiny.add_(1.0), flush)
     return {"rows": rows, "floor_us": round(floor * 1e6, 2),
-            "method": ("gpu_us: mean of 30 eager launches, each queued behind an L2 flush "
-                       "(256 MB write + 256 MB read: cold, clean L2), CUDA events; C4 = one "
-                       "batched launch for all 512 subdomains; gpu_frac: algorithmic bytes / "
-                       "time / MEASURED_PEAKS hbm_gbs; floor_us: same for a 1-element kernel")}
+            "method": ("gpu_us: mean of 30 eager bound launches (bind_program / bind_batch: "
+                       "one C call, host cost hidden behind the flush), each queued behind an "
+                       "L2 flush (256 MB write + 256 MB read: cold, clean L2), CUDA events; C4 "
+                       "= one batched launch for all 512 subdomains; gpu_frac: algorithmic "
+                       "bytes / time / MEASURED_PEAKS hbm_gbs; floor_us: same for a 1-element "
+                       "kernel (event + launch overhead included in every gpu_us)")}
 
 
 def run_reference(args, dist: Dist) -> dict | None:

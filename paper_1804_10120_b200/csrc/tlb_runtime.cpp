@@ -348,7 +348,8 @@ struct tlb_kernel {
   std::vector<long long> slot_comp;
   std::vector<int> slot_flags;
   int threads = 256;   // compiled TLK_THREADS: default block size (from the source)
-  int stage_threads = 0;  // block size (= tile) of tlk_stage_v1 (from the source)
+  int stage_threads = 0;  // tile (points) of tlk_stage_v1 (from the source)
+  int stage_block = 0;    // its block: the tile, + a producer warp when TLK_STAGE_WS
   int stage_smem = 0;     // its dynamic shared memory (from the source)
   int stage_batch_smem = 0;  // tlk_stage_batch_v1's: the ring + NSTAGE x NSLOTS pointers
   std::mutex mu;
@@ -382,7 +383,7 @@ int load_module(tlb_kernel* k, CUcontext ctx, Loaded** out) {
     int block = k->threads, smem = 0;
     if (e == STAGE_V1 || e == STAGE_BATCH_V1) {
       smem = e == STAGE_V1 ? k->stage_smem : k->stage_batch_smem;
-      block = k->stage_threads + (e == STAGE_BATCH_V1 ? 32 : 0);
+      block = e == STAGE_V1 ? k->stage_block : k->stage_threads + 32;
       if (smem <= 0 ||
           g_cu.ModuleGetFunction(&L.fn[e], L.mod, kEntryNames[e]) != CUDA_SUCCESS) {
         L.fn[e] = nullptr;
@@ -496,6 +497,9 @@ int tlb_compile(const char* src, const char* const* opts, int nopts, const char*
     k->stage_threads = (int)source_define(src, "TLK_STAGE_THREADS", 128);
     if (k->stage_threads < 32 || k->stage_threads > 1024 || k->stage_threads % 32)
       return fail("tlb_compile: TLK_STAGE_THREADS %d is not a block size", k->stage_threads);
+    k->stage_block = k->stage_threads + (source_define(src, "TLK_STAGE_WS", 0) ? 32 : 0);
+    if (k->stage_block > 1024)
+      return fail("tlb_compile: staged block of %d threads", k->stage_block);
     const long long smem =
         nstage * source_define(src, "TLK_NREAD", 1) * k->stage_threads * 8;
     if (smem > 227 * 1024) return fail("tlb_compile: staged tile ring of %lld bytes", smem);
@@ -614,10 +618,11 @@ int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n, const uint6
   memcpy(&param[1], slots, m * sizeof(uint64_t));
   if (threads <= 0) threads = k->threads;
   if (stage) {
-    // persistent: one block per resident slot, each walks whole tiles; the
-    // block is the tile (the compiled TLK_STAGE_THREADS)
-    threads = k->stage_threads;
-    long long tiles = std::max(1LL, n / threads);
+    // persistent: one block per resident slot, each walks whole tiles of the
+    // compiled TLK_STAGE_THREADS points (block: the tile, + a producer warp
+    // in the warp-specialised form)
+    threads = k->stage_block;
+    long long tiles = std::max(1LL, n / k->stage_threads);
     long long blocks = std::min<long long>(tiles, (long long)st->sm_count * L->occ[STAGE_V1]);
     if (max_blocks > 0) blocks = std::min(blocks, max_blocks);
     void* args[] = {param.data()};

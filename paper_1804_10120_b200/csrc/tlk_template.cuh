@@ -277,6 +277,104 @@ __device__ __forceinline__ unsigned tlk_smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
 
+#ifndef TLK_STAGE_WS
+#define TLK_STAGE_WS 0
+#endif
+#if TLK_STAGE_WS
+// Warp-specialised form (TLK_STAGE_WS 1): block = TLK_STAGE_THREADS consumer
+// threads + one producer warp.  Lane 0 of the producer waits on the stage's
+// `empty` barrier (one arrival per consumer warp), then re-arms `full` with
+// the tile's byte count and issues its bulk copies; consumer warps release a
+// stage as soon as they are done with it — no block-wide barrier per tile, and
+// no consumer thread serialises the copy issue.
+extern "C" __global__ void __launch_bounds__(TLK_STAGE_THREADS + 32)
+tlk_stage_v1(const tlk_flat_params prm) {
+  constexpr int kRord[TLK_NSLOTS] = TLK_RORD;
+  constexpr int kTile = TLK_STAGE_THREADS;
+  constexpr int kWarps = TLK_STAGE_THREADS / 32;
+  extern __shared__ __align__(128) double tlk_sm[];  // [NSTAGE][NREAD][kTile]
+  __shared__ __align__(8) unsigned long long full[TLK_NSTAGE], empty[TLK_NSTAGE];
+  const long long ntiles = prm.n / kTile;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < TLK_NSTAGE; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tlk_smem_addr(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tlk_smem_addr(&empty[s])),
+                   "r"(kWarps));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid >= kTile) {  // producer warp: lane 0 issues, the other lanes exit
+    if (tid != kTile) return;
+#if TLK_L2HINT
+    const unsigned long long pol = tl_evict_first_policy();
+#endif
+    int it = 0;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int s = it % TLK_NSTAGE;
+      if (it >= TLK_NSTAGE) {
+        const unsigned eb = tlk_smem_addr(&empty[s]);
+        const unsigned ph = (unsigned)(it / TLK_NSTAGE - 1) & 1u;
+        asm volatile(
+            "{\n .reg .pred p;\n"
+            "TLK_EWAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            " @!p bra TLK_EWAIT_%=;\n}" ::"r"(eb), "r"(ph) : "memory");
+      }
+      const unsigned b = tlk_smem_addr(&full[s]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                   ::"r"(b), "r"((unsigned)(TLK_NREAD * kTile * sizeof(double))) : "memory");
+#pragma unroll
+      for (int j = 0; j < TLK_NSLOTS; ++j) {
+        if (kRord[j] < 0) continue;
+        const double* src = prm.p[j] + t * kTile;
+        double* dst = tlk_sm + ((long long)s * TLK_NREAD + kRord[j]) * kTile;
+#if TLK_L2HINT
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+            "[%0], [%1], %2, [%3], %4;"
+            ::"r"(tlk_smem_addr(dst)), "l"(src), "r"((unsigned)(kTile * sizeof(double))), "r"(b),
+              "l"(pol)
+            : "memory");
+#else
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(tlk_smem_addr(dst)), "l"(src), "r"((unsigned)(kTile * sizeof(double))), "r"(b)
+            : "memory");
+#endif
+      }
+    }
+    return;
+  }
+  int it = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % TLK_NSTAGE;
+    const unsigned phase = (unsigned)(it / TLK_NSTAGE) & 1u;
+    const unsigned b = tlk_smem_addr(&full[s]);
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "TLK_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra TLK_WAIT_%=;\n}" ::"r"(b), "r"(phase) : "memory");
+    tlk_flat_params q;
+    q.n = prm.n;
+#pragma unroll
+    for (int j = 0; j < TLK_NSLOTS; ++j)
+      q.p[j] = kRord[j] >= 0 ? tlk_sm + ((long long)s * TLK_NREAD + kRord[j]) * kTile
+                             : prm.p[j] + t * kTile;
+    tlk_point<double, 3>(q, tid);
+    __syncwarp();  // the warp's reads of stage s are done
+    if ((tid & 31) == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tlk_smem_addr(&empty[s]))
+                   : "memory");
+  }
+  const long long stride = (long long)gridDim.x * kTile;
+  for (long long x = ntiles * kTile + (long long)blockIdx.x * kTile + tid; x < prm.n;
+       x += stride)
+    tlk_point<double>(prm, x);
+}
+#else
 extern "C" __global__ void __launch_bounds__(TLK_STAGE_THREADS)
 tlk_stage_v1(const tlk_flat_params prm) {
   constexpr int kRord[TLK_NSLOTS] = TLK_RORD;
@@ -361,6 +459,7 @@ tlk_stage_v1(const tlk_flat_params prm) {
        x += stride)
     tlk_point<double>(prm, x);
 }
+#endif  // TLK_STAGE_WS
 
 // tlk_stage_batch_v1: the multi-domain batch through the same ring, with a
 // dedicated producer warp (block = TLK_STAGE_THREADS consumers + 32).  Work

@@ -476,6 +476,7 @@ class Variant:
     stage_threads: int = 128  # TLK_STAGE_THREADS: the staged entry's block = tile (points)
     stage_reads: int = 0  # read slots copied through the ring (0 = all; the rest load directly)
     minb: int = 0  # TLK_MINB: min resident blocks/SM of the flat entries (0 = unconstrained)
+    stage_ws: int = 0  # TLK_STAGE_WS: staged entry with a dedicated producer warp (1) or not (0)
 
     def tag(self) -> str:
         t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
@@ -485,6 +486,7 @@ class Variant:
         t += f"g{self.stage}x{self.stage_threads}" if self.stage else ""
         t += f"r{self.stage_reads}" if self.stage and self.stage_reads else ""
         t += f"m{self.minb}" if self.minb else ""
+        t += "p" if self.stage and self.stage_ws else ""
         return t + (f"n{self.threads}" if self.threads != 256 else "")
 
     def small_class(self) -> "Variant":
@@ -508,9 +510,10 @@ class Variant:
         """Whether two variants compile to the same cubin (vec/waves are
         launch-time choices; both entry points are in every module)."""
         return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs, self.stage,
-                 self.threads, self.stage_threads, self.stage_reads, self.minb)
+                 self.threads, self.stage_threads, self.stage_reads, self.minb, self.stage_ws)
                 == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs, other.stage,
-                    other.threads, other.stage_threads, other.stage_reads, other.minb))
+                    other.threads, other.stage_threads, other.stage_reads, other.minb,
+                    other.stage_ws))
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -625,6 +628,8 @@ def _env_variant(v: Variant) -> Variant:
         kw["stage_reads"] = int(env["TLK_STAGE_READS"])
     if "TLK_MINB" in env:
         kw["minb"] = int(env["TLK_MINB"])
+    if "TLK_STAGE_WS" in env:
+        kw["stage_ws"] = int(env["TLK_STAGE_WS"])
     if kw:
         kw["small_n"] = 0  # a forced variant applies at every size ...
     if "TLK_SMALL_N" in env:
@@ -725,6 +730,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         header.append(f"#define TLK_NREAD {len(rord) - rord.count(-1)}")
         header.append(f"#define TLK_STAGE_THREADS {variant.stage_threads}")
         header.append("#define TLK_RORD {" + ",".join(map(str, rord)) + "}")
+        if variant.stage_ws:
+            header.append("#define TLK_STAGE_WS 1")
         if variant.batch_vec == 3:
             header.append("#define TLK_STAGE_BATCH 1")
     header.append(f"#define TLK_LDMODE {variant.ldmode}")

@@ -1,6 +1,9 @@
 """One program at one size, launched a few times (an ncu target).
-Usage: PYTHONPATH=. python scripts/ncu_target.py PROGRAM LOG2N"""
+Usage: python scripts/ncu_target.py PROGRAM LOG2N"""
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch
 

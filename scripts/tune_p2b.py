@@ -80,6 +80,13 @@ def main():
         ("r36", Variant(**{**v0.__dict__, "stage_reads": 36}), ""),
         ("r36_s3x256_l2hint", Variant(**{**v0.__dict__, "stage_reads": 36}), "-DTLK_L2HINT=1"),
         ("stmode1_l2hint", v0, "-DTLK_STMODE=1 -DTLK_L2HINT=1"),
+        ("ws", Variant(**{**v0.__dict__, "stage_ws": 1}), ""),
+        ("ws_r36", Variant(**{**v0.__dict__, "stage_ws": 1, "stage_reads": 36}), ""),
+        ("ws_r40_s4x128", Variant(**{**v0.__dict__, "stage_ws": 1, "stage_reads": 40,
+                                     "stage": 4, "stage_threads": 128}), ""),
+        ("ws_r40_s2x256", Variant(**{**v0.__dict__, "stage_ws": 1, "stage_reads": 40,
+                                     "stage": 2}), ""),
+        ("ws_l2hint", Variant(**{**v0.__dict__, "stage_ws": 1}), "-DTLK_L2HINT=1"),
         ("policy_again", v0, ""),
     ]
     only = os.environ.get("SHAPES")

@@ -176,6 +176,11 @@ def main():
                         {}),
         "t256_s4_r12": (Variant(**{**v3.__dict__, "small_n": 0, "stage": 4, "stage_reads": 12}),
                         {}),
+        "ws": (Variant(**{**v3.__dict__, "small_n": 0, "stage_ws": 1}), {}),
+        "ws_t128_s4": (Variant(**{**v3.__dict__, "small_n": 0, "stage_ws": 1,
+                                  "stage_threads": 128, "stage": 4}), {}),
+        "ws_r24_s2": (Variant(**{**v3.__dict__, "small_n": 0, "stage_ws": 1, "stage": 2,
+                                 "stage_reads": 24}), {}),
         "plain_v2": (Variant(**{**v3.__dict__, "small_n": 0, "stage": 0}), {"vec": 2}),
         "plain_v1_w4": (Variant(**{**v3.__dict__, "small_n": 0, "stage": 0}),
                         {"vec": 1, "max_blocks": -4}),

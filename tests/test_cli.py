@@ -79,14 +79,15 @@ def test_eval_writes_the_reference_container(case, per_component, tmp_path):
 
 @pytest.mark.gpu
 def test_eval_stops_where_the_reference_stops(tmp_path):
-    # reference cli.py:93-99: an EvalError part-way through the program is a
-    # diagnostic (exit 2, "<file>: <message>"), and no output is written
+    # reference cli.py:96-102: an EvalError part-way through the program is a
+    # diagnostic (EXIT_DIAGNOSTICS = 1, "<file>: <message>"), and no output is
+    # written
     spec = manifest()["cases"]["error_after_first_statement"]
     f = tmp_path / "p.tl"
     f.write_text(spec["source"])
     out = tmp_path / "out.tldf"
     res = _cli("eval", str(f), "--data", str(GOLDEN / "error_after_first_statement.in.tldf"),
                "--out", str(out))
-    assert res.returncode == 2
+    assert res.returncode == 1
     assert res.stderr == f"{f}: {spec['raises']['message']}\n"
     assert not out.exists()

@@ -225,6 +225,18 @@ def test_reference_harness_drives_the_gpu_kernels(case, tmp_path):
     got, want = read_host(out), golden_io(case)[1]
     for t in spec["targets"]:
         assert same_bits(got[t], want[t]), t
+    # and the reference's own comparator agrees, bitwise and in its rtol mode
+    # (tl_compare.c:26-64; run_tests.sh's differential checks use both)
+    compare = refc.REF_DIR / "tl_compare"
+    if compare.exists():
+        gold = GOLDEN / f"{case}.out.tldf"
+        modes = [[str(out), str(gold), "1e-13"]]
+        if case != "special_values":  # NaN payloads differ between x86 and the GPU
+            modes.append(["--bitwise", str(out), str(gold)])
+        for args in modes:
+            res = subprocess.run([str(compare), *args], capture_output=True, text=True,
+                                 timeout=120)
+            assert res.returncode == 0, (args, res.stdout, res.stderr)
 
 
 def test_bound_launch_fast_path_tracks_storage():
@@ -290,7 +302,8 @@ def test_fuzzed_programs_match_oracle(seed):
 
 VARIANTS = [dict(restrict=False), dict(hoist=True), dict(vec=1), dict(ldmode=1),
             dict(hoist=True, ldmode=1, vec=1), dict(waves=4), dict(stage=2),
-            dict(stage=3, hoist=True), dict(stage=3, stage_reads=2)]
+            dict(stage=3, hoist=True), dict(stage=3, stage_reads=2),
+            dict(stage=3, stage_reads=2, stage_ws=1)]
 
 
 @pytest.mark.parametrize("vkw", VARIANTS, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()))
@@ -466,8 +479,9 @@ def test_size_classes_bitwise_at_the_boundary(name):
 
 
 @pytest.mark.parametrize("name", ["c1_dtg", "c2_maxwell", "c3_christoffel", "p2", "p3"])
-@pytest.mark.parametrize("stage,reads", [(2, 0), (4, 0), (3, 5)])
-def test_tma_staged_entry_bitwise(name, stage, reads):
+@pytest.mark.parametrize("stage,reads,ws", [(2, 0, 0), (4, 0, 0), (3, 5, 0), (2, 0, 1),
+                                           (3, 5, 1)])
+def test_tma_staged_entry_bitwise(name, stage, reads, ws):
     # many whole tiles per block (ring wrap-around, mbarrier phase flips), a
     # ragged tail, and an unaligned slab view (falls back to the plain entry)
     from paper_1804_10120_b200 import bench as tb
@@ -481,7 +495,7 @@ def test_tma_staged_entry_bitwise(name, stage, reads):
         env = tb.make_env(prog, targets[0], n, 0xC0FFEE)
         host = {k: f.data.cpu().numpy().copy() for k, f in env.items()}
         _, _, stores = _bind(vs, env)
-        plan = lower_program(vs, variant=Variant(stage=stage, stage_reads=reads))
+        plan = lower_program(vs, variant=Variant(stage=stage, stage_reads=reads, stage_ws=ws))
         if plan.variant.stage == 0:
             pytest.skip("read-modify-write program: no staged entry")
         k = Kernel(plan)
