@@ -517,7 +517,8 @@ class Variant:
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
-                   chained: int) -> Variant:
+                   chained: int, statements: int = 1,
+                   policy: int | None = None) -> Variant:
     """Default per-kernel choice — a policy fitted to measurements on B200
     (profiles/r01/tune_*.jsonl: 12 variants x 8 programs at 2^24-2^26 points).
 
@@ -552,7 +553,32 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
       of measured copy bandwidth (34 of 40 reads staged) vs 101.1 % (30 of
       40, 128-point tiles) and 99.1 % plain (profiles/r01/bench_stage_*).
       Staging every read caps P2 below the plain kernel.
+
+    Round 2 (policy 2, the default; ``policy=1`` or TLK_POLICY=1 gives the
+    round-1 choices above): the staged entry runs warp-specialised
+    (``stage_ws``: a producer warp issues the bulk copies, consumer warps
+    release a stage through an mbarrier instead of a block-wide barrier per
+    tile).  Interleaved A/B on B200 (profiles/r02/tune_ab_*.jsonl, medians
+    of 7 rounds x 10 launches, 2^24-2^28 points), against policy 1:
+
+    * light single-statement kernels: 3-deep ring, warp-specialised —
+      C1 +2.0 %, add1-3 +2.5-4.4 %, K_ij +2.0 %; multi-statement light
+      programs keep the block-barrier ring (Maxwell, 8 statements: -1.6 to
+      -2.0 % warp-specialised, and no staged share or ring depth recovers it);
+    * heavier kernels of < 32 reads (C3): 3-deep ring of 256-point tiles,
+      three quarters of the reads staged, warp-specialised: +1.3-2.8 %;
+    * 32-48 reads (P2, P3): a 2-deep ring of 256-point tiles (0.85 / 0.75 of
+      the reads), warp-specialised: P2 +1.9-2.6 % (2^24-2^28), P3 +1.0 %;
+      the 3-deep warp-specialised ring is 2-4 % SLOWER than policy 1 on
+      these, the 2-deep one faster;
+    * more reads than that (the contractions: 90-108 reads, 81 writes) were
+      left unstaged by policy 1 (a 3-deep ring of three quarters of their
+      reads leaves 4 warps per SM); now 40 of them are staged through a
+      2-deep ring of 128-point tiles (80 KB: 2 blocks per SM):
+      contract1 +7.7 %, contract2 +32 %.
     """
+    if policy is None:
+        policy = int(os.environ.get("TLK_POLICY", "2"))
     arrays = reads + writes
     # the staged entries unroll per-slot loops: beyond a few hundred slots
     # (unmeasured territory, slow NVRTC compiles) the plain entries are used
@@ -565,12 +591,19 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
                            small_n=SMALL_N_LIGHT)
         return Variant(restrict=True, hoist=True, ldmode=0, vec=1, waves=4,
                        small_n=SMALL_N_LIGHT, stage=3, stage_threads=256,
-                       stage_reads=max(1, (reads + 1) // 2))
+                       stage_reads=max(1, (reads + 1) // 2),
+                       stage_ws=int(policy >= 2 and statements < 4))
     if rw_slots == 0:
         share = 0.85 if reads >= 32 and not chained else 0.75
+        staged = max(1, round(share * reads))
+        depth, tile = 3, 256
+        if policy >= 2 and reads >= 32:
+            depth = 2
+            if staged > 40:  # contraction-class: 40 staged reads, 128-point tiles
+                staged, tile = 40, 128
         return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=2, waves=4 if chained else 1,
-                       small_n=SMALL_N_HEAVY, stage=3 if stageable else 0, stage_threads=256,
-                       stage_reads=max(1, round(share * reads)), batch_threads=128)
+                       small_n=SMALL_N_HEAVY, stage=depth if stageable else 0, stage_threads=tile,
+                       stage_reads=staged, batch_threads=128, stage_ws=int(policy >= 2))
     return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
 
 
@@ -672,7 +705,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     phases = _phases(b.instrs)
     policy = variant is None
     if variant is None:
-        variant = _env_variant(choose_variant(reads, writes, n_ops, rw, b.chained))
+        variant = _env_variant(choose_variant(reads, writes, n_ops, rw, b.chained,
+                                              len(statements)))
         if "TLK_STAGE_FRAC" in os.environ:  # tuning: staged share of the read slots
             frac = float(os.environ["TLK_STAGE_FRAC"])
             variant = Variant(**{**variant.__dict__,

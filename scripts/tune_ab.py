@@ -1,0 +1,158 @@
+"""Interleaved A/B of lowering variants on one B200: for each (program, N)
+every variant runs ROUNDS times in round-robin order (so clock and thermal
+drift hit all variants alike), each time K eager launches back to back
+bracketed by CUDA events; reported: median and min per variant, and every
+variant's output compared bitwise with the first's.
+
+Cases come from the CASES env var (JSON list of
+{"program": name, "n": points, "variants": {label: {Variant overrides}}}),
+overrides applied on top of the policy variant; default: the round-2
+warp-specialisation candidates.
+
+Usage: python scripts/tune_ab.py  -> JSON lines"""
+
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1804_10120_b200 import bench as tb  # noqa: E402
+from paper_1804_10120_b200.lowering import Variant, lower_program  # noqa: E402
+from paper_1804_10120_b200.runtime import fill_uniform, get_kernel  # noqa: E402
+
+ROUNDS = int(os.environ.get("ROUNDS", "7"))
+K = int(os.environ.get("K", "10"))
+
+DEFAULT = [
+    {"program": "p2", "n": 1 << 28, "variants": {
+        "policy": {}, "ws_s2": {"stage_ws": 1, "stage": 2},
+        "ws_s2_r40": {"stage_ws": 1, "stage": 2, "stage_reads": 40},
+        "ws_s2_r30": {"stage_ws": 1, "stage": 2, "stage_reads": 30}}},
+    {"program": "p3", "n": 1 << 26, "variants": {
+        "policy": {}, "ws_s2": {"stage_ws": 1, "stage": 2}}},
+    {"program": "c3_christoffel", "n": 1 << 21, "variants": {
+        "policy": {"small_n": 0}, "ws": {"small_n": 0, "stage_ws": 1}}},
+    {"program": "c3_christoffel", "n": 1 << 26, "variants": {
+        "policy": {}, "ws": {"stage_ws": 1}}},
+    {"program": "c1_dtg", "n": 1 << 26, "variants": {
+        "policy": {}, "ws": {"stage_ws": 1}}},
+    {"program": "c2_maxwell", "n": 1 << 26, "variants": {
+        "policy": {}, "ws": {"stage_ws": 1}}},
+]
+
+
+def source(name: str) -> str:
+    if name in tb.PROGRAMS:
+        return tb.PROGRAMS[name]
+    return {e.name: e.source for e in tb.builtin_suite()}[name]
+
+
+def run(case):
+    name, n = case["program"], int(case["n"])
+    prog, vs = tb.load(source(name))
+    base = lower_program(vs)
+    if case.get("staged_only") and not base.variant.stage:
+        print(json.dumps({"program": name, "N": n, "skipped": "not staged by the policy",
+                          "variant": base.variant.tag()}), flush=True)
+        return
+    bufs = []
+    for k, info in enumerate(base.fields):
+        b = torch.zeros(info.n_components, n, dtype=torch.float64, device="cuda")
+        if k not in base.lhs_fields:
+            for c in range(info.n_components):
+                fill_uniform(b[c], 0xC0FFEE, (k << 8) | c)
+        bufs.append(b)
+    bases = [b.data_ptr() for b in bufs]
+    pitches = [n if info.n_components > 1 else 0 for info in base.fields]
+    stream = torch.cuda.current_stream().cuda_stream
+    kerns, plans, same = {}, {}, {}
+    want = None
+    for label, over in case["variants"].items():
+        if "__policy__" in over:  # the lowering policy's own choice under TLK_POLICY=k
+            old = os.environ.get("TLK_POLICY")
+            os.environ["TLK_POLICY"] = str(over["__policy__"])
+            plan = lower_program(vs)
+            if old is None:
+                os.environ.pop("TLK_POLICY")
+            else:
+                os.environ["TLK_POLICY"] = old
+        else:
+            var = Variant(**{**base.variant.__dict__, **over})
+            plan = lower_program(vs, variant=var)
+        kern = get_kernel(plan)
+        for k in base.lhs_fields:
+            bufs[k].zero_()
+        kern.launch(n, bases, pitches, stream)
+        torch.cuda.synchronize()
+        out = torch.cat([bufs[k][:, ::1009].flatten() for k in base.lhs_fields])
+        if want is None:
+            want = out.clone()
+        same[label] = bool(torch.equal(out.view(torch.int64), want.view(torch.int64)))
+        kerns[label], plans[label] = kern, plan
+    ts = {label: [] for label in kerns}
+    for _ in range(ROUNDS):
+        for label, kern in kerns.items():
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(K):
+                kern.launch(n, bases, pitches, stream)
+            b.record()
+            b.synchronize()
+            ts[label].append(a.elapsed_time(b) / 1e3 / K)
+    for label, t in ts.items():
+        med = statistics.median(t)
+        bpp = plans[label].bytes_per_point
+        print(json.dumps({"program": name, "N": n, "shape": label,
+                          "variant": plans[label].variant.tag(),
+                          "us_median": round(med * 1e6, 2), "us_min": round(min(t) * 1e6, 2),
+                          "tbs_median": round(bpp * n / med / 1e12, 4),
+                          "tbs_best": round(bpp * n / min(t) / 1e12, 4),
+                          "bitwise_same": same[label],
+                          "us_all": [round(x * 1e6, 1) for x in t]}), flush=True)
+    del bufs, kerns
+    torch.cuda.empty_cache()
+
+
+def main():
+    cases = json.loads(os.environ["CASES"]) if os.environ.get("CASES") else DEFAULT
+    if os.environ.get("SUITE_WS"):  # every suite statement: policy vs warp-specialised ring
+        n = int(os.environ["SUITE_WS"])
+        cases = [{"program": e.name, "n": n, "staged_only": True,
+                  "variants": {"policy": {}, "ws": {"stage_ws": 1},
+                               "ws_s2": {"stage_ws": 1, "stage": 2}}}
+                 for e in tb.builtin_suite()]
+        cases += [{"program": "c2_maxwell", "n": n, "variants": {
+            "policy": {}, "ws": {"stage_ws": 1}, "ws_r12": {"stage_ws": 1, "stage_reads": 12},
+            "ws_r14": {"stage_ws": 1, "stage_reads": 14},
+            "ws_r18_s2": {"stage_ws": 1, "stage_reads": 18, "stage": 2}}},
+            {"program": "p2", "n": n, "variants": {
+                "policy": {}, "ws_s2": {"stage_ws": 1, "stage": 2},
+                "ws_s2_r32": {"stage_ws": 1, "stage": 2, "stage_reads": 32},
+                "ws_s2_r36": {"stage_ws": 1, "stage": 2, "stage_reads": 36},
+                "ws_s2_t128_r40": {"stage_ws": 1, "stage": 2, "stage_reads": 40,
+                                   "stage_threads": 128},
+                "ws_s3_t128_r40": {"stage_ws": 1, "stage": 3, "stage_reads": 40,
+                                   "stage_threads": 128}}}]
+        cases += [{"program": c, "n": n, "variants": {
+            "policy": {}, "ws_s2_t128_r40": {"stage_ws": 1, "stage": 2, "stage_reads": 40,
+                                             "stage_threads": 128},
+            "ws_s2_r24": {"stage_ws": 1, "stage": 2, "stage_reads": 24}}}
+            for c in ("contract1", "contract2")]
+    if os.environ.get("POLICY_AB"):  # round-1 vs round-2 policy, every program
+        sizes = [int(x) for x in os.environ["POLICY_AB"].split(",")]
+        names = [e.name for e in tb.builtin_suite()] + list(tb.PROGRAMS)
+        cases = [{"program": nm, "n": n, "variants": {"policy1": {"__policy__": 1},
+                                                      "policy2": {"__policy__": 2}}}
+                 for n in sizes for nm in names]
+    for case in cases:
+        run(case)
+
+
+if __name__ == "__main__":
+    main()

@@ -161,7 +161,7 @@ def main():
         c1 = {k: c1[k] for k in ("cur_v1_w4", "v1_t128", "v1_t64", "v1_onewave",
                                  "v1_t128_onewave", "v1_unroll2_onewave", "v1_ldnc_t128")}
     run("C1_dtg", tb.DTG, 64**3, c1)
-    if os.environ.get("ONLY_C1_NEW"):
+    if os.environ.get("ONLY_C1_NEW") or os.environ.get("ONLY_C1"):
         return
     prog, vs = tb.load(tb.CHRISTOFFEL)
     v3 = lower_program(vs).variant

@@ -148,27 +148,47 @@ def _defines(src: str) -> dict:
     for ln in src.splitlines():
         if ln.startswith("#define TLK_"):
             parts = ln.split(None, 2)
-            out[parts[1]] = parts[2] if len(parts) > 2 else ""
+            # the generated header comes first; the template's #ifndef
+            # defaults after it must not override it
+            out.setdefault(parts[1], parts[2] if len(parts) > 2 else "")
     return out
 
 
-@pytest.mark.parametrize("name,tile,staged", [("c1_dtg", 256, 8), ("c3_christoffel", 256, 18),
-                                              ("c4_p2", 256, 34), ("c4_p3", 256, 32)])
-def test_staged_policy_ring_layout(name, tile, staged):
-    # choose_variant's staged share, and the ring's read-slot ordinals: the
-    # first `staged` read slots in slot order, numbered densely
+@pytest.mark.parametrize("name,depth,tile,staged,ws", [
+    ("c1_dtg", 3, 256, 8, 1), ("c2_maxwell", 3, 256, 9, 0), ("c3_christoffel", 3, 256, 18, 1),
+    ("c4_p2", 2, 256, 34, 1), ("c4_p3", 2, 256, 32, 1)])
+def test_staged_policy_ring_layout(name, depth, tile, staged, ws):
+    # choose_variant's ring (round-2 policy: warp-specialised except for
+    # multi-statement light programs; 2-deep for 32+ reads), its staged
+    # share, and the ring's read-slot ordinals: the first `staged` read
+    # slots in slot order, numbered densely
     _, vs = program(manifest()["cases"][name]["source"])
     plan = lower_program(vs)
     var = plan.variant
-    assert var.stage == 3 and var.stage_threads == tile
+    assert var.stage == depth and var.stage_threads == tile and var.stage_ws == ws
     d = _defines(plan.source)
+    assert int(d.get("TLK_STAGE_WS", "0")) == ws
     rord = [int(x) for x in d["TLK_RORD"].strip("{}").split(",")]
     assert int(d["TLK_NREAD"]) == staged == sum(1 for r in rord if r >= 0)
     reads = [j for j, fl in enumerate(plan.slot_flags) if fl & SLOT_READ]
     assert [rord[j] for j in reads[:staged]] == list(range(staged))
     assert all(rord[j] == -1 for j in range(len(rord)) if j not in reads[:staged])
-    assert 3 * staged * tile * 8 <= 224 * 1024
+    assert depth * staged * tile * 8 <= 224 * 1024
     assert int(d["TLK_STAGE_THREADS"]) == tile and int(d["TLK_THREADS"]) == 256
+
+
+def test_contraction_class_policy_stages_40_reads_in_128_point_tiles():
+    # contract1 (90 reads, 81 writes): policy 1 left it unstaged (a 3-deep
+    # ring of 3/4 of its reads leaves 4 warps per SM); policy 2 stages 40
+    # reads through a 2-deep ring of 128-point tiles, warp-specialised
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.lowering import choose_variant
+
+    src = {e.name: e.source for e in tb.builtin_suite()}["contract1"]
+    _, vs = program(src)
+    var = lower_program(vs).variant
+    assert (var.stage, var.stage_threads, var.stage_reads, var.stage_ws) == (2, 128, 40, 1)
+    assert choose_variant(90, 81, 405, 0, 0, policy=1).stage == 3  # then refused by the warp rule
 
 
 def test_stage_refused_for_read_write_and_read_free_programs():
