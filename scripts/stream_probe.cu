@@ -70,6 +70,55 @@ __global__ void __launch_bounds__(256) probe_copy1(const double* __restrict__ a,
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     st1<MODE>(b + i, __ldcs(a + i));
 }
+// 256-bit accesses (LDG/STG.E.ENL2.256, sm_100) and non-persistent grids
+// (one block per 256 x vector chunk, no stride loop — torch's elementwise shape)
+__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d) : "memory");
+}
+__global__ void __launch_bounds__(256) probe_write_v4(double* __restrict__ a, long long n4) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
+    st4(a + 4 * i, 1.0, 2.0, 3.0, 4.0);
+}
+__global__ void __launch_bounds__(256) probe_write_np(double* __restrict__ a, long long n, int w) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w == 4) {
+    if (4 * i < n) st4(a + 4 * i, 1.0, 2.0, 3.0, 4.0);
+  } else if (w == 2) {
+    if (2 * i < n) *reinterpret_cast<double2*>(a + 2 * i) = make_double2(1.0, 2.0);
+  } else {
+    if (i < n) a[i] = 1.0;
+  }
+}
+__global__ void __launch_bounds__(256) probe_copy_np(const double* __restrict__ a,
+                                                     double* __restrict__ b, long long n, int w) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w == 4) {
+    if (4 * i < n) {
+      double x, y, z, q;
+      asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                   : "=d"(x), "=d"(y), "=d"(z), "=d"(q) : "l"(a + 4 * i));
+      st4(b + 4 * i, x, y, z, q);
+    }
+  } else if (w == 2) {
+    if (2 * i < n)
+      reinterpret_cast<double2*>(b)[i] = __ldg(reinterpret_cast<const double2*>(a) + i);
+  } else {
+    if (i < n) b[i] = __ldg(a + i);
+  }
+}
+__global__ void __launch_bounds__(256) probe_copy_v4(const double* __restrict__ a,
+                                                     double* __restrict__ b, long long n4) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    double x, y, z, q;
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(x), "=d"(y), "=d"(z), "=d"(q) : "l"(a + 4 * i));
+    st4(b + 4 * i, x, y, z, q);
+  }
+}
+
 // TMA bulk store: each block fills a smem chunk once, then streams it out
 template <int CH>
 __global__ void __launch_bounds__(128) probe_bulk_store(char* __restrict__ a, long long bytes) {
@@ -193,6 +242,27 @@ int sp_copy1(const void* a, void* b, long long n, int blocks_per_sm, void* strea
   else if (mode == 1) probe_copy1<1><<<g, 256, 0, s>>>((const double*)a, (double*)b, n);
   else if (mode == 2) probe_copy1<2><<<g, 256, 0, s>>>((const double*)a, (double*)b, n);
   else probe_copy1<4><<<g, 256, 0, s>>>((const double*)a, (double*)b, n);
+  return (int)cudaGetLastError();
+}
+int sp_write_v4(void* a, long long n, int blocks_per_sm, void* stream) {
+  probe_write_v4<<<sms() * blocks_per_sm, 256, 0, (cudaStream_t)stream>>>((double*)a, n / 4);
+  return (int)cudaGetLastError();
+}
+int sp_write_np(void* a, long long n, int w, void* stream) {
+  long long threads = (n + w - 1) / w;
+  probe_write_np<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>((double*)a,
+                                                                                     n, w);
+  return (int)cudaGetLastError();
+}
+int sp_copy_np(const void* a, void* b, long long n, int w, void* stream) {
+  long long threads = (n + w - 1) / w;
+  probe_copy_np<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (const double*)a, (double*)b, n, w);
+  return (int)cudaGetLastError();
+}
+int sp_copy_v4(const void* a, void* b, long long n, int blocks_per_sm, void* stream) {
+  probe_copy_v4<<<sms() * blocks_per_sm, 256, 0, (cudaStream_t)stream>>>((const double*)a,
+                                                                        (double*)b, n / 4);
   return (int)cudaGetLastError();
 }
 int sp_bulk_store(void* a, long long bytes, int blocks_per_sm, void* stream) {

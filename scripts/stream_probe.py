@@ -71,6 +71,14 @@ def main():
         rec("write_tma_bulk_store", 8 * n, t, chunk=8192, blocks_per_sm=bps)
     t = timeit(lambda: a.fill_(1.5))
     rec("write_torch_fill", 8 * n, t)
+    for bps in (4, 8):
+        t = timeit(lambda: lib.sp_write_v4(ctypes.c_void_p(a.data_ptr()), ctypes.c_longlong(n),
+                                           bps, st))
+        rec("write", 8 * n, t, store="st.global.v4.f64 (256-bit)", width=32, blocks_per_sm=bps)
+    for w in (1, 2, 4):
+        t = timeit(lambda: lib.sp_write_np(ctypes.c_void_p(a.data_ptr()), ctypes.c_longlong(n),
+                                           w, st))
+        rec("write_nonpersistent_grid", 8 * n, t, width=8 * w)
     half = n // 2
     src, dst = a[:half], a[half:2 * half]
     for mode, mname in modes.items():
@@ -81,6 +89,16 @@ def main():
             rec("copy_8B_per_thread", 16 * half, t, store=mname, blocks_per_sm=bps)
     t = timeit(lambda: dst.copy_(src))
     rec("copy_torch", 16 * half, t)
+    for w in (1, 2, 4):
+        t = timeit(lambda: lib.sp_copy_np(ctypes.c_void_p(src.data_ptr()),
+                                          ctypes.c_void_p(dst.data_ptr()),
+                                          ctypes.c_longlong(half), w, st))
+        rec("copy_nonpersistent_grid", 16 * half, t, width=8 * w)
+    for bps in (4, 8):
+        t = timeit(lambda: lib.sp_copy_v4(ctypes.c_void_p(src.data_ptr()),
+                                          ctypes.c_void_p(dst.data_ptr()),
+                                          ctypes.c_longlong(half), bps, st))
+        rec("copy_v4_persistent", 16 * half, t, width=32, blocks_per_sm=bps)
     del a
     torch.cuda.empty_cache()
     # stream mixes: m points per stream, nr + nw streams
