@@ -44,6 +44,11 @@ extern "C" {
 
 #define TLB_ABI_VERSION 1
 
+/* tlb_launch max_blocks at or above this: a one-shot grid (one block per
+ * `threads` points or point pairs, no grid-stride trips; small launches get
+ * smaller blocks so every SM has work) */
+#define TLB_ONE_SHOT (1LL << 62)
+
 /* slot flags for tlb_kernel_set_slots */
 #define TLB_SLOT_READ 1
 #define TLB_SLOT_WRITE 2
@@ -103,7 +108,8 @@ int tlb_kernel_attrs(tlb_kernel* k, const char* entry, int* regs, int* local_byt
  * falls back to the 1-point entry when a slot is not 16-byte aligned).
  * threads: block size (0 = the kernel's compiled TLK_THREADS; must not
  * exceed it).  max_blocks: grid cap (0 = one full wave at occupancy, -w = w
- * waves).  Asynchronous on `stream`. */
+ * waves, > 0 that many blocks at most, >= TLB_ONE_SHOT a one-shot grid).
+ * Asynchronous on `stream`. */
 int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
                const long long* pitches, int vec, int threads, long long max_blocks,
                void* stream);

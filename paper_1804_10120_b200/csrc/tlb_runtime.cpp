@@ -350,6 +350,11 @@ struct tlb_kernel {
   int threads = 256;   // compiled TLK_THREADS: default block size (from the source)
   int stage_threads = 0;  // tile (points) of tlk_stage_v1 (from the source)
   int stage_block = 0;    // its block: the tile, + a producer warp when TLK_STAGE_WS
+  // default launch geometry of the flat entry for callers that do not pass
+  // one (tlb_exec_host, the harness bindings): TLK_GRID_WAVES (0 = one-shot
+  // grid, w = w waves) and TLK_VEC (1 or 2 points per thread) from the source
+  int dflt_waves = 1;
+  int dflt_vec = 2;
   int stage_smem = 0;     // its dynamic shared memory (from the source)
   int stage_batch_smem = 0;  // tlk_stage_batch_v1's: the ring + NSTAGE x NSLOTS pointers
   std::mutex mu;
@@ -490,6 +495,8 @@ int tlb_compile(const char* src, const char* const* opts, int nopts, const char*
   // launch geometry from the source: block size, and the staged entry's
   // tile ring (TLK_NSTAGE x TLK_NREAD x TLK_THREADS doubles)
   k->threads = (int)source_define(src, "TLK_THREADS", 256);
+  k->dflt_waves = (int)source_define(src, "TLK_GRID_WAVES", 1);
+  k->dflt_vec = (int)source_define(src, "TLK_VEC", 2) == 1 ? 1 : 2;
   const long long nstage = source_define(src, "TLK_NSTAGE", 0);
   if (k->threads < 32 || k->threads > 1024 || k->threads % 32)
     return fail("tlb_compile: TLK_THREADS %d is not a block size", k->threads);
@@ -622,9 +629,12 @@ int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n, const uint6
     // compiled TLK_STAGE_THREADS points (block: the tile, + a producer warp
     // in the warp-specialised form)
     threads = k->stage_block;
+    // (max_blocks > 0: that many blocks, at most one per tile — e.g. one
+    // block per tile, a one-shot grid instead of a persistent one)
     long long tiles = std::max(1LL, n / k->stage_threads);
-    long long blocks = std::min<long long>(tiles, (long long)st->sm_count * L->occ[STAGE_V1]);
-    if (max_blocks > 0) blocks = std::min(blocks, max_blocks);
+    long long blocks = max_blocks > 0
+                           ? std::min(tiles, max_blocks)
+                           : std::min<long long>(tiles, (long long)st->sm_count * L->occ[STAGE_V1]);
     void* args[] = {param.data()};
     CU(g_cu.LaunchKernel(L->fn[STAGE_V1], (unsigned)blocks, 1, 1, (unsigned)threads, 1, 1,
                          (unsigned)k->stage_smem, stream, args, nullptr),
@@ -634,6 +644,13 @@ int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n, const uint6
   const int e = vec2 ? FLAT_V2 : FLAT_V1;
   long long units = vec2 ? n / 2 : n;
   if (units < 1) units = 1;
+  if (max_blocks >= TLB_ONE_SHOT && units < (long long)st->sm_count * 4 * threads) {
+    // one-shot grid of a small launch: smaller blocks, so that every SM
+    // gets ~4 of them (a 512-thread block per 512 points would leave most
+    // SMs idle below ~300K points)
+    const long long per = (units + st->sm_count * 4 - 1) / (st->sm_count * 4);
+    threads = (int)std::max(64LL, std::min<long long>(threads, (per + 31) / 32 * 32));
+  }
   long long blocks = (units + threads - 1) / threads;
   // max_blocks > 0: explicit cap; 0: one full wave at occupancy; -w: w waves
   int occ = L->occ[e];
@@ -643,7 +660,7 @@ int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n, const uint6
   }
   long long waves = max_blocks < 0 ? -max_blocks : 1;
   long long cap = max_blocks > 0 ? max_blocks : (long long)st->sm_count * occ * waves;
-  blocks = std::max(1LL, std::min(blocks, cap));
+  blocks = std::max(1LL, std::min(std::min(blocks, cap), 0x7fffffffLL));
   void* args[] = {param.data()};
   CU(g_cu.LaunchKernel(L->fn[e], (unsigned)blocks, 1, 1, (unsigned)threads, 1, 1, 0, stream,
                        args, nullptr),
@@ -869,7 +886,12 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
         CU(g_cu.MemcpyHtoDAsync(slots[j], src, (size_t)cnt * sizeof(double), s), "H2D");
       }
     }
-    if (launch_flat(k, L, st, cnt, slots.data(), true, 0, 0, s)) return 1;
+    // the kernel's own launch geometry (staging buffers are 16-byte aligned)
+    if (launch_flat(k, L, st, cnt, slots.data(), k->dflt_vec == 2, 0,
+                    k->dflt_waves == 0 ? TLB_ONE_SHOT
+                                       : (k->dflt_waves > 1 ? -k->dflt_waves : 0),
+                    s))
+      return 1;
     for (size_t j = 0; j < m; ++j) {
       if (k->slot_flags[j] & TLB_SLOT_WRITE) {
         double* dst = const_cast<double*>(comp_ptrs[k->slot_field[j]][k->slot_comp[j]]) + lo;

@@ -459,7 +459,9 @@ class Variant:
               when no slot is both read and written (a load could otherwise
               sink below a later store of its own slot), enforced here
     vec       2 = two points per thread step (128-bit accesses), 1 = one
-    waves     grid = waves x SMs x resident blocks (grid-stride loop)
+    waves     grid = waves x SMs x resident blocks (grid-stride loop); 0 = a
+              one-shot grid: one block per `threads` points (pairs), every
+              thread one loop trip (lowering policy 3)
     """
 
     restrict: bool = True
@@ -504,6 +506,8 @@ class Variant:
           staged entry is ahead (profiles/r01/r01t/tune_smalln.jsonl)."""
         if self.vec == 1 and not self.stage:
             return Variant(**{**self.__dict__, "hoist": True, "small_n": 0})
+        if self.waves == 0 and not self.stage:  # one-shot grids are already one wave here
+            return Variant(**{**self.__dict__, "vec": 1, "small_n": 0})
         return Variant(**{**self.__dict__, "vec": 1, "waves": 4, "small_n": 0})
 
     def same_code(self, other: "Variant") -> bool:
@@ -578,8 +582,10 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
       contract1 +7.7 %, contract2 +32 %.
     """
     if policy is None:
-        policy = int(os.environ.get("TLK_POLICY", "2"))
+        policy = int(os.environ.get("TLK_POLICY", "3"))
     arrays = reads + writes
+    if policy >= 3:
+        return _policy3(reads, writes, n_ops, rw_slots, chained)
     # the staged entries unroll per-slot loops: beyond a few hundred slots
     # (unmeasured territory, slow NVRTC compiles) the plain entries are used
     # write-dominated programs stream better through the plain entries
@@ -605,6 +611,48 @@ def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
                        small_n=SMALL_N_HEAVY, stage=depth if stageable else 0, stage_threads=tile,
                        stage_reads=staged, batch_threads=128, stage_ws=int(policy >= 2))
     return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
+
+
+def _policy3(reads: int, writes: int, n_ops: int, rw_slots: int, chained: int) -> Variant:
+    """Lowering policy 3 (round 2, the default): every kernel is the plain
+    per-point entry over a ONE-SHOT grid (``waves=0``: one block per
+    `threads` points, no grid-stride loop).  Persistent grid-stride grids —
+    the plain entries' 1-4 waves and the TMA-staged entry's persistent ring
+    alike — lose 2-36 % to it on this part: in interleaved A/B runs
+    (profiles/r02/tuning/tune_ab_oneshot_*.jsonl, 2^21 and 2^26 points) the
+    one-shot flat entry beats policy 2 (warp-specialised TMA rings) on C1
+    +2.4 %, Maxwell +2.9 %, C3 +3-4 %, P2 +1.4-3.5 %, P3 +4-5 %, K_ij
+    +6.5 %, contract1 +5 %, and the write-dominated programs the most
+    (outer3 +36 %, assign3 +21 % at 2^26).  The device's own streaming probes
+    agree (scripts/stream_probe.cu): pure writes 7.61 TB/s one-shot vs
+    5.9-6.3 TB/s persistent with every store flavour, 256-bit stores and TMA
+    bulk stores; copies 6.97 vs 6.08 TB/s.
+
+    * light (<= 1.5 ops per streamed array, copies and the write-dominated
+      outer products included): 1 point per thread, 512-thread blocks, every
+      load hoisted to the top of the body — at 2^21-2^26 points the best of
+      8 launch shapes on every write-dominated program
+      (profiles/r02/tuning/tune_ab_write_dominated.jsonl: outer3 +66 %,
+      assign1 +23 %, assign3 +21 %, outer1 +10 %, outer2 +8 % over policy
+      2), and no size class: below ~300K points the runtime shrinks a
+      one-shot grid's blocks so every SM gets ~4 (tlb_runtime launch_flat);
+    * heavier: 1 point per thread, 128-thread blocks (register-heavy
+      bodies: finer block granularity — P2 +0.3-4 %, P3 +17-23 %, contract1
+      +3-4 % over 256 threads);
+    * read-modify-write slots: as policy 2 (2 points per thread, 4 waves,
+      no restrict).
+    Loads stay as fitted in round 1 (hoisted for light and chained programs,
+    movable ld.global.nc for heavier read-only ones).  The TMA-staged entry
+    remains available as a variant (``stage``), bit-exact and tested."""
+    arrays = reads + writes
+    if rw_slots:
+        return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
+    if n_ops <= 1.5 * arrays:
+        return Variant(restrict=True, hoist=True, ldmode=0, vec=1, waves=0, threads=512)
+    # (no size class: a one-shot grid of 1-point threads is already the
+    # round-1 small-N choice for heavier kernels)
+    return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=1, waves=0, threads=128,
+                   batch_threads=128)
 
 
 # dynamic shared memory budget of the staged entry's tile ring (bytes; the
@@ -757,6 +805,10 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         header.append("// " + _statement_comment(v))
     header.append(f"#define TLK_NSLOTS {n_slots}")
     header.append(f"#define TLK_THREADS {variant.threads}")
+    # default flat-entry launch geometry for C-ABI callers that pass none
+    # (tlb_exec_host: the host-staged path and the harness bindings)
+    header.append(f"#define TLK_GRID_WAVES {variant.waves}")
+    header.append(f"#define TLK_VEC {variant.vec}")
     if variant.minb:
         header.append(f"#define TLK_MINB {variant.minb}")
     if variant.stage:

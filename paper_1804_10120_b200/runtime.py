@@ -212,8 +212,8 @@ class Kernel:
         self.vec = 1 if (var is not None and var.vec == 1) else 0
         if var is not None and var.stage:
             self.vec = 3  # the staged entry (its tile ring size is read from the source)
-        if var is not None and var.waves > 1 and self.max_blocks == 0:
-            self.max_blocks = -var.waves
+        if var is not None and self.max_blocks == 0:
+            self.max_blocks = _grid_cap(var.waves)
         # batch entry: 0 = 2-point when aligned, 1 = 1-point, 3 = TMA-staged
         self.batch_vec = 1 if (var is not None and var.batch_vec == 1) else 0
         if var is not None and var.batch_vec == 3:
@@ -231,8 +231,7 @@ class Kernel:
         self.small_n = small_n
         self.small = small
         self.small_vec = 1 if sv.vec == 1 else 0
-        self.small_max_blocks = (-sv.waves if sv.waves > 1 else 0) if self.max_blocks <= 0 \
-            else self.max_blocks
+        self.small_max_blocks = _grid_cap(sv.waves)
 
     @property
     def log(self) -> str:
@@ -296,6 +295,20 @@ class Kernel:
         check(lib().tlb_exec_host(self.handle, n, outer, slab, stream), "tlb_exec_host")
         self.launches += 1
         _pin(self)
+
+
+# tlb_launch's max_blocks for a one-shot grid: a cap no launch reaches, so the
+# grid is one block per `threads` points (pairs) — the runtime clamps it to
+# the 2^31-1 grid limit, beyond which the grid-stride loop covers the rest
+ONE_SHOT = 1 << 62
+
+
+def _grid_cap(waves: int) -> int:
+    """tlb_launch max_blocks for Variant.waves: 0 one-shot, 1 one wave at
+    occupancy, w > 1 w waves."""
+    if waves == 0:
+        return ONE_SHOT
+    return -waves if waves > 1 else 0
 
 
 def address_arrays(bases: Sequence[int], pitches: Sequence[int]):

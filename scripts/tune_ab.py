@@ -71,7 +71,7 @@ def run(case):
     bases = [b.data_ptr() for b in bufs]
     pitches = [n if info.n_components > 1 else 0 for info in base.fields]
     stream = torch.cuda.current_stream().cuda_stream
-    kerns, plans, same = {}, {}, {}
+    kerns, plans, same, launch_kw = {}, {}, {}, {}
     want = None
     for label, over in case["variants"].items():
         if "__policy__" in over:  # the lowering policy's own choice under TLK_POLICY=k
@@ -83,12 +83,20 @@ def run(case):
             else:
                 os.environ["TLK_POLICY"] = old
         else:
-            var = Variant(**{**base.variant.__dict__, **over})
+            var = Variant(**{**base.variant.__dict__,
+                             **{k: v for k, v in over.items() if not k.startswith("__")}})
             plan = lower_program(vs, variant=var)
         kern = get_kernel(plan)
+        lk = dict(over.get("__launch__", {}))
+        if lk.get("max_blocks") == "all":  # non-persistent: one thread per point (pair)
+            lk["max_blocks"] = -(-n // (lk.get("vec", 1) * kern.threads))
+        elif isinstance(lk.get("max_blocks"), str) and lk["max_blocks"].startswith("tiles"):
+            per = int(lk["max_blocks"][5:] or 1)  # "tilesK": K tiles per staged block
+            lk["max_blocks"] = max(1, n // plan.variant.stage_threads // per)
+        launch_kw[label] = lk
         for k in base.lhs_fields:
             bufs[k].zero_()
-        kern.launch(n, bases, pitches, stream)
+        kern.launch(n, bases, pitches, stream, **lk)
         torch.cuda.synchronize()
         out = torch.cat([bufs[k][:, ::1009].flatten() for k in base.lhs_fields])
         if want is None:
@@ -101,7 +109,7 @@ def run(case):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             for _ in range(K):
-                kern.launch(n, bases, pitches, stream)
+                kern.launch(n, bases, pitches, stream, **launch_kw[label])
             b.record()
             b.synchronize()
             ts[label].append(a.elapsed_time(b) / 1e3 / K)
@@ -147,9 +155,55 @@ def main():
     if os.environ.get("POLICY_AB"):  # round-1 vs round-2 policy, every program
         sizes = [int(x) for x in os.environ["POLICY_AB"].split(",")]
         names = [e.name for e in tb.builtin_suite()] + list(tb.PROGRAMS)
-        cases = [{"program": nm, "n": n, "variants": {"policy1": {"__policy__": 1},
-                                                      "policy2": {"__policy__": 2}}}
+        pa, pb = os.environ.get("POLICY_PAIR", "1,2").split(",")
+        cases = [{"program": nm, "n": n, "variants": {f"policy{pa}": {"__policy__": int(pa)},
+                                                      f"policy{pb}": {"__policy__": int(pb)}}}
                  for n in sizes for nm in names]
+    if os.environ.get("ONESHOT"):  # one-shot grids: flat entry shapes vs staged entry
+        sizes = [int(x) for x in os.environ["ONESHOT"].split(",")]
+        names = os.environ.get("PROGS", "c1_dtg,c2_maxwell,c3_christoffel,p2,p3,kij,"
+                                        "contract1,outer3,assign3").split(",")
+        cases = []
+        for n in sizes:
+            for nm in names:
+                v = {"policy": {},
+                     "v1_np": {"stage": 0, "__launch__": {"vec": 1, "max_blocks": "all"}},
+                     "v1_np_t128": {"stage": 0, "threads": 128,
+                                    "__launch__": {"vec": 1, "max_blocks": "all"}},
+                     "v1_np_t512": {"stage": 0, "threads": 512,
+                                    "__launch__": {"vec": 1, "max_blocks": "all"}},
+                     "v2_np": {"stage": 0, "__launch__": {"vec": 2, "max_blocks": "all"}}}
+                if lower_program(tb.load(source(nm))[1]).variant.stage:
+                    v["staged_np1"] = {"__launch__": {"vec": 3, "max_blocks": "tiles1"}}
+                    v["staged_np4"] = {"__launch__": {"vec": 3, "max_blocks": "tiles4"}}
+                cases.append({"program": nm, "n": n, "variants": v})
+    if os.environ.get("WRITEDOM"):  # write-dominated / copy programs: launch shapes
+        sizes = [int(x) for x in os.environ["WRITEDOM"].split(",")]
+        cases = []
+        for n in sizes:
+            for nm in ("outer1", "outer2", "outer3", "assign1", "assign3"):
+                cases.append({"program": nm, "n": n, "variants": {
+                    "p2_v1_w4_t256": {"__policy__": 2},
+                    "v1_w4_t256_h1": {"vec": 1, "waves": 4, "threads": 256, "hoist": True,
+                                      "small_n": 0},
+                    "v1_np_t256": {"vec": 1, "waves": 0, "threads": 256, "small_n": 0},
+                    "v1_np_t512": {"vec": 1, "waves": 0, "threads": 512, "small_n": 0},
+                    "v1_np_t512_h1": {"vec": 1, "waves": 0, "threads": 512, "hoist": True,
+                                      "small_n": 0},
+                    "v2_np_t256": {"vec": 2, "waves": 0, "threads": 256, "small_n": 0},
+                    "v2_np_t512": {"vec": 2, "waves": 0, "threads": 512, "small_n": 0},
+                    "v2_w4_t256": {"vec": 2, "waves": 4, "threads": 256, "small_n": 0}}})
+    if os.environ.get("NONPERSISTENT"):  # grid-stride vs one-shot grids of the flat entries
+        n = int(os.environ["NONPERSISTENT"])
+        names = ["assign1", "assign3", "outer1", "outer3", "add3", "kij", "c1_dtg", "c2_maxwell",
+                 "c3_christoffel", "p2", "contract1"]
+        cases = [{"program": nm, "n": n, "variants": {
+            "policy": {},
+            "flat_v1_w4": {"stage": 0, "__launch__": {"vec": 1, "max_blocks": -4}},
+            "flat_v1_np": {"stage": 0, "__launch__": {"vec": 1, "max_blocks": "all"}},
+            "flat_v2_w1": {"stage": 0, "__launch__": {"vec": 2, "max_blocks": 0}},
+            "flat_v2_np": {"stage": 0, "__launch__": {"vec": 2, "max_blocks": "all"}}}}
+            for nm in names]
     for case in cases:
         run(case)
 

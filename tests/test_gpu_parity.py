@@ -457,10 +457,10 @@ def test_batch_entry_variants_bit_exact(name, bptrs, bvec):
 
 
 @pytest.mark.parametrize("name", ["c1_dtg", "c2_maxwell", "c3_christoffel", "p2", "p3"])
-def test_size_classes_bitwise_at_the_boundary(name):
-    # launches of <= small_n points run Variant.small_class() (a hoisted
-    # second cubin for light kernels, 1 point/thread for heavier ones);
-    # both sides of the boundary must be bit-identical to the oracle
+def test_one_shot_block_shrink_bitwise_at_the_boundary(name):
+    # a one-shot launch of fewer than SMs x 4 x threads points runs smaller
+    # blocks (tlb_runtime launch_flat); both sides of that boundary, and
+    # tiny launches, must be bit-identical to the oracle
     from paper_1804_10120_b200 import bench as tb
     from paper_1804_10120_b200.evaluator import kernel_for
 
@@ -468,14 +468,9 @@ def test_size_classes_bitwise_at_the_boundary(name):
     targets = [v.stmt.lhs.field for v in vs]
     env = tb.make_env(prog, targets[0], 8, 0xC0FFEE)
     kern = kernel_for(vs, env)
-    assert kern.small_n > 0
-    var = kern.plan.variant
-    if var.stage:
-        # staged above small_n, the same cubin's 1-point entry below
-        assert kern.vec == 3 and kern.small is None and kern.small_vec == 1
-    elif var.vec == 1:
-        assert kern.small is not None and kern.small.plan.variant.hoist
-    for n in (kern.small_n - 1, kern.small_n, kern.small_n + 3):
+    assert kern.max_blocks == 1 << 62  # one-shot
+    edge = torch.cuda.get_device_properties(0).multi_processor_count * 4 * kern.threads
+    for n in (1, 63, 1000, edge - 1, edge, edge + 3):
         env = tb.make_env(prog, targets[0], n, 0xC0FFEE)
         host = {k: f.data.cpu().numpy().copy() for k, f in env.items()}
         eval_program(vs, env)
@@ -619,7 +614,9 @@ def test_suite_statements_under_the_default_policy_at_large_n(name):
 
     src = {e.name: e.source for e in tb.builtin_suite()}[name]
     prog, vs = program(src)
-    n = 128 * 148 * 2 * 5 + 77 if name.startswith("contract") else (1 << 21) + 333
+    # contractions: just past the heavier size class (2^20), 28 128-point
+    # tiles per block; the others past the light class (2^21)
+    n = 128 * 148 * 2 * 28 + 77 if name.startswith("contract") else (1 << 21) + 333
     host = random_host_env(prog, n, 11)
     want = {k: a.copy() for k, a in host.items()}
     numpy_eval.eval_program(vs, want)
@@ -631,8 +628,23 @@ def test_suite_statements_under_the_default_policy_at_large_n(name):
     kern = kernel_for(vs, env)
     assert n > kern.small_n
     if name.startswith("contract"):
-        var = kern.plan.variant
+        # and policy 2's contraction-class ring (2-deep, 128-point tiles, 40
+        # staged reads, warp-specialised) on the same inputs
+        from paper_1804_10120_b200.evaluator import _bind
+        from paper_1804_10120_b200.lowering import choose_variant, lower_program
+        from paper_1804_10120_b200.runtime import Kernel
+
+        p3 = kern.plan
+        var = choose_variant(p3.reads, p3.writes, p3.n_ops, 0, 0, policy=2)
         assert (var.stage, var.stage_threads, var.stage_reads, var.stage_ws) == (2, 128, 40, 1)
+        env2 = device_env(prog, host)
+        _, _, stores = _bind(vs, env2)
+        k2 = Kernel(lower_program(vs, variant=var))
+        k2.launch(n, [s_.base for s_ in stores], [s_.pitch for s_ in stores],
+                  torch.cuda.current_stream().cuda_stream)
+        got2 = env_to_host(env2)
+        for k in want:
+            assert same_bits(got2[k], want[k]), ("policy 2 ring", k)
 
 
 def test_bound_launches_and_batch_fast_path():

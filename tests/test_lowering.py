@@ -157,11 +157,12 @@ def _defines(src: str) -> dict:
 @pytest.mark.parametrize("name,depth,tile,staged,ws", [
     ("c1_dtg", 3, 256, 8, 1), ("c2_maxwell", 3, 256, 9, 0), ("c3_christoffel", 3, 256, 18, 1),
     ("c4_p2", 2, 256, 34, 1), ("c4_p3", 2, 256, 32, 1)])
-def test_staged_policy_ring_layout(name, depth, tile, staged, ws):
-    # choose_variant's ring (round-2 policy: warp-specialised except for
-    # multi-statement light programs; 2-deep for 32+ reads), its staged
-    # share, and the ring's read-slot ordinals: the first `staged` read
-    # slots in slot order, numbered densely
+def test_staged_policy_ring_layout(name, depth, tile, staged, ws, monkeypatch):
+    # policy 2's ring (warp-specialised except for multi-statement light
+    # programs; 2-deep for 32+ reads), its staged share, and the ring's
+    # read-slot ordinals: the first `staged` read slots in slot order,
+    # numbered densely
+    monkeypatch.setenv("TLK_POLICY", "2")
     _, vs = program(manifest()["cases"][name]["source"])
     plan = lower_program(vs)
     var = plan.variant
@@ -177,18 +178,47 @@ def test_staged_policy_ring_layout(name, depth, tile, staged, ws):
     assert int(d["TLK_STAGE_THREADS"]) == tile and int(d["TLK_THREADS"]) == 256
 
 
-def test_contraction_class_policy_stages_40_reads_in_128_point_tiles():
+def test_contraction_class_policy_stages_40_reads_in_128_point_tiles(monkeypatch):
     # contract1 (90 reads, 81 writes): policy 1 left it unstaged (a 3-deep
     # ring of 3/4 of its reads leaves 4 warps per SM); policy 2 stages 40
     # reads through a 2-deep ring of 128-point tiles, warp-specialised
     from paper_1804_10120_b200 import bench as tb
     from paper_1804_10120_b200.lowering import choose_variant
 
+    monkeypatch.setenv("TLK_POLICY", "2")
+
     src = {e.name: e.source for e in tb.builtin_suite()}["contract1"]
     _, vs = program(src)
     var = lower_program(vs).variant
     assert (var.stage, var.stage_threads, var.stage_reads, var.stage_ws) == (2, 128, 40, 1)
     assert choose_variant(90, 81, 405, 0, 0, policy=1).stage == 3  # then refused by the warp rule
+
+
+@pytest.mark.parametrize("name,vec,threads,hoist,ldmode", [
+    ("c1_dtg", 1, 512, True, 0), ("c2_maxwell", 1, 512, True, 0),
+    ("c3_christoffel", 1, 128, False, 1), ("c4_p2", 1, 128, False, 1),
+    ("c4_p3", 1, 128, True, 1), ("suite_outer3", 1, 512, True, 0),
+    ("suite_assign3", 1, 512, True, 0), ("suite_contract1", 1, 128, False, 1)])
+def test_default_policy_is_one_shot_flat(name, vec, threads, hoist, ldmode):
+    # policy 3 (the default): the plain entry over a one-shot grid, no TMA
+    # ring, no size class; the launch geometry travels in the source for
+    # C-ABI callers that pass none (tlb_exec_host, the harness bindings)
+    _, vs = program(manifest()["cases"][name]["source"])
+    plan = lower_program(vs)
+    var = plan.variant
+    assert (var.stage, var.waves, var.vec, var.threads, var.hoist, var.ldmode, var.small_n) == \
+        (0, 0, vec, threads, hoist, ldmode, 0)
+    d = _defines(plan.source)
+    assert d["TLK_GRID_WAVES"] == "0" and d["TLK_VEC"] == str(vec)
+    assert d["TLK_THREADS"] == str(threads) and "TLK_NSTAGE" not in d
+    k = get_kernel(plan)
+    assert k.max_blocks == 1 << 62 and k.vec == 1 and k.small is None
+
+
+def test_read_modify_write_programs_keep_the_two_point_waves():
+    _, vs = program("tensor A dim 3 rank 1;\ntensor B dim 3 rank 1;\nA(i) += B(i);\n")
+    var = lower_program(vs).variant
+    assert (var.vec, var.waves, var.restrict) == (2, 4, False)
 
 
 def test_stage_refused_for_read_write_and_read_free_programs():
@@ -214,13 +244,18 @@ def test_stage_ring_clamped_to_shared_memory():
 
 
 @pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="no cuobjdump")
-def test_staged_entries_use_bulk_copies_without_spills():
+@pytest.mark.parametrize("ws", [0, 1])
+def test_staged_entries_use_bulk_copies_without_spills(ws):
+    from paper_1804_10120_b200.lowering import Variant
+
     _, vs = program(manifest()["cases"]["c4_p2"]["source"])
-    k = get_kernel(lower_program(vs))
+    # the staged entry is a variant (policy 3 does not pick it; policy 2 did)
+    k = get_kernel(lower_program(vs, variant=Variant(stage=2, stage_threads=256,
+                                                     stage_reads=34, stage_ws=ws, ldmode=1)))
     sass = _sass(k)
     # the staged batch entry is opt-in (measured slower): not in default modules
     assert "tlk_stage_v1" in sass and "tlk_stage_batch_v1" not in sass
-    from paper_1804_10120_b200.lowering import Variant
+    assert "tlk_stage_v1" not in _sass(get_kernel(lower_program(vs)))
 
     opt = get_kernel(lower_program(vs, variant=Variant(stage=3, batch_vec=3)))
     assert "tlk_stage_batch_v1" in _sass(opt)
