@@ -355,6 +355,7 @@ struct tlb_kernel {
   // grid, w = w waves) and TLK_VEC (1 or 2 points per thread) from the source
   int dflt_waves = 1;
   int dflt_vec = 2;
+  int batch_bound = 256;  // TLK_BATCH_BOUND: the batch entries' largest block
   int stage_smem = 0;     // its dynamic shared memory (from the source)
   int stage_batch_smem = 0;  // tlk_stage_batch_v1's: the ring + NSTAGE x NSLOTS pointers
   std::mutex mu;
@@ -385,7 +386,9 @@ int load_module(tlb_kernel* k, CUcontext ctx, Loaded** out) {
   Loaded L;
   CU(g_cu.ModuleLoadData(&L.mod, k->cubin.data()), "cuModuleLoadData");
   for (int e = 0; e < N_ENTRIES; ++e) {
-    int block = k->threads, smem = 0;
+    int block = (e == BATCH_V1 || e == BATCH_V2) ? std::min(k->threads, k->batch_bound)
+                                                  : k->threads,
+        smem = 0;
     if (e == STAGE_V1 || e == STAGE_BATCH_V1) {
       smem = e == STAGE_V1 ? k->stage_smem : k->stage_batch_smem;
       block = e == STAGE_V1 ? k->stage_block : k->stage_threads + 32;
@@ -482,10 +485,19 @@ int tlb_device_sm_count(int* out) {
 
 // Value of `#define NAME <int>` in a generated source (lowering.py writes the
 // launch geometry there), or `dflt`.
+// A numeric `#define NAME value` of the generated header.  Only the header
+// is searched (it ends where the template's own text begins), so the
+// template's `#ifndef NAME / #define NAME <fallback expression>` defaults
+// never shadow an absent header define; a non-numeric value also yields
+// `dflt`.
 long long source_define(const char* src, const char* name, long long dflt) {
   const std::string key = std::string("#define ") + name + " ";
+  const char* end = strstr(src, "// tlk_template.cuh");
   const char* p = strstr(src, key.c_str());
-  return p ? atoll(p + key.size()) : dflt;
+  if (!p || (end && p > end)) return dflt;
+  const char* v = p + key.size();
+  if (!(*v == '-' || (*v >= '0' && *v <= '9'))) return dflt;
+  return atoll(v);
 }
 
 int tlb_compile(const char* src, const char* const* opts, int nopts, const char* cache_path,
@@ -495,6 +507,7 @@ int tlb_compile(const char* src, const char* const* opts, int nopts, const char*
   // launch geometry from the source: block size, and the staged entry's
   // tile ring (TLK_NSTAGE x TLK_NREAD x TLK_THREADS doubles)
   k->threads = (int)source_define(src, "TLK_THREADS", 256);
+  k->batch_bound = (int)source_define(src, "TLK_BATCH_BOUND", k->threads);
   k->dflt_waves = (int)source_define(src, "TLK_GRID_WAVES", 1);
   k->dflt_vec = (int)source_define(src, "TLK_VEC", 2) == 1 ? 1 : 2;
   const long long nstage = source_define(src, "TLK_NSTAGE", 0);
@@ -780,7 +793,10 @@ int tlb_batch_launch(tlb_batch* b, int vec, int threads, void* stream) {
   if (vec == 3) vec = 1;  // no staged batch entry: the 1-point batch entry
   const bool v2 = b->vec2 && vec != 1;
   const int e = v2 ? BATCH_V2 : BATCH_V1;
-  if (threads <= 0) threads = b->k->threads;
+  if (threads <= 0) threads = std::min(b->k->threads, b->k->batch_bound);
+  if (threads > b->k->batch_bound)
+    return fail("tlb_batch_launch: %d threads exceed the batch entry's bound %d", threads,
+                b->k->batch_bound);
   long long units = v2 ? (b->max_n + 1) / 2 : b->max_n;
   long long gx = std::max(1LL, (units + threads - 1) / threads);
   long long gy = std::min<long long>(b->ndom, 65535);

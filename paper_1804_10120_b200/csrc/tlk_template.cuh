@@ -244,12 +244,17 @@ __device__ __forceinline__ void tlk_batch_body(const long long* __restrict__ tab
 #endif
 }
 
-extern "C" __global__ void __launch_bounds__(TLK_THREADS)
+// the batch entries' own launch bound (lowering: TLK_BATCH_BOUND, default
+// the flat entries' TLK_THREADS); their blocks are at most this large
+#ifndef TLK_BATCH_BOUND
+#define TLK_BATCH_BOUND TLK_THREADS
+#endif
+extern "C" __global__ void __launch_bounds__(TLK_BATCH_BOUND)
 tlk_batch_v1(const long long* __restrict__ table, int ndom) {
   tlk_batch_body<double>(table, ndom);
 }
 
-extern "C" __global__ void __launch_bounds__(TLK_THREADS)
+extern "C" __global__ void __launch_bounds__(TLK_BATCH_BOUND)
 tlk_batch_v2(const long long* __restrict__ table, int ndom) {
   tlk_batch_body<double2>(table, ndom);
 }

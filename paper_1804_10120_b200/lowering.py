@@ -479,6 +479,7 @@ class Variant:
     stage_reads: int = 0  # read slots copied through the ring (0 = all; the rest load directly)
     minb: int = 0  # TLK_MINB: min resident blocks/SM of the flat entries (0 = unconstrained)
     stage_ws: int = 0  # TLK_STAGE_WS: staged entry with a dedicated producer warp (1) or not (0)
+    batch_bound: int = 0  # TLK_BATCH_BOUND: the batch entries' __launch_bounds__ (0 = threads)
 
     def tag(self) -> str:
         t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
@@ -489,6 +490,7 @@ class Variant:
         t += f"r{self.stage_reads}" if self.stage and self.stage_reads else ""
         t += f"m{self.minb}" if self.minb else ""
         t += "p" if self.stage and self.stage_ws else ""
+        t += f"q{self.batch_bound}" if self.batch_bound else ""
         return t + (f"n{self.threads}" if self.threads != 256 else "")
 
     def small_class(self) -> "Variant":
@@ -514,10 +516,11 @@ class Variant:
         """Whether two variants compile to the same cubin (vec/waves are
         launch-time choices; both entry points are in every module)."""
         return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs, self.stage,
-                 self.threads, self.stage_threads, self.stage_reads, self.minb, self.stage_ws)
+                 self.threads, self.stage_threads, self.stage_reads, self.minb, self.stage_ws,
+                 self.batch_bound)
                 == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs, other.stage,
                     other.threads, other.stage_threads, other.stage_reads, other.minb,
-                    other.stage_ws))
+                    other.stage_ws, other.batch_bound))
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -647,12 +650,17 @@ def _policy3(reads: int, writes: int, n_ops: int, rw_slots: int, chained: int) -
     arrays = reads + writes
     if rw_slots:
         return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
+    # the multi-domain batch entries are unchanged from policy 2 (256-thread
+    # launch bounds; 256- / 128-thread blocks): the flat entries' block size
+    # must not change their code (P2's batch entry compiled for 128-thread
+    # bounds took 88 instead of 106 registers and ran C4 in 173 vs 160 us)
     if n_ops <= 1.5 * arrays:
-        return Variant(restrict=True, hoist=True, ldmode=0, vec=1, waves=0, threads=512)
+        return Variant(restrict=True, hoist=True, ldmode=0, vec=1, waves=0, threads=512,
+                       batch_threads=256, batch_bound=256)
     # (no size class: a one-shot grid of 1-point threads is already the
     # round-1 small-N choice for heavier kernels)
     return Variant(restrict=True, hoist=chained > 0, ldmode=1, vec=1, waves=0, threads=128,
-                   batch_threads=128)
+                   batch_threads=128, batch_bound=256)
 
 
 # dynamic shared memory budget of the staged entry's tile ring (bytes; the
@@ -811,6 +819,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     header.append(f"#define TLK_VEC {variant.vec}")
     if variant.minb:
         header.append(f"#define TLK_MINB {variant.minb}")
+    if variant.batch_bound:
+        header.append(f"#define TLK_BATCH_BOUND {variant.batch_bound}")
     if variant.stage:
         header.append(f"#define TLK_NSTAGE {variant.stage}")
         header.append(f"#define TLK_NREAD {len(rord) - rord.count(-1)}")

@@ -1,7 +1,10 @@
 """BASELINE configs as ncu targets (final policy): C1 64^3, C3 128^3,
 C2 Maxwell 10^8, C4 P2 and P3 chain (512 x 16^3, one batched launch).
-Usage: PYTHONPATH=. python scripts/ncu_configs.py CONFIG"""
+Usage: python scripts/ncu_configs.py CONFIG"""
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch
 

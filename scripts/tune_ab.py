@@ -177,6 +177,21 @@ def main():
                     v["staged_np1"] = {"__launch__": {"vec": 3, "max_blocks": "tiles1"}}
                     v["staged_np4"] = {"__launch__": {"vec": 3, "max_blocks": "tiles4"}}
                 cases.append({"program": nm, "n": n, "variants": v})
+    if os.environ.get("HEAVY"):  # policy-3 heavier kernels: load flavour, hoist, register cap
+        sizes = [int(x) for x in os.environ["HEAVY"].split(",")]
+        cases = []
+        for n in sizes:
+            for nm in os.environ.get("PROGS", "c3_christoffel,p2,p3,contract1").split(","):
+                cases.append({"program": nm, "n": n, "variants": {
+                    "policy3": {},
+                    "hoist": {"hoist": True},
+                    "ldcs": {"ldmode": 0},
+                    "minb4": {"minb": 4},
+                    "minb6": {"minb": 6},
+                    "minb8": {"minb": 8},
+                    "t64": {"threads": 64},
+                    "t256_minb3": {"threads": 256, "minb": 3},
+                    "v2_t128": {"vec": 2, "__launch__": {"vec": 2}}}})
     if os.environ.get("WRITEDOM"):  # write-dominated / copy programs: launch shapes
         sizes = [int(x) for x in os.environ["WRITEDOM"].split(",")]
         cases = []
