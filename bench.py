@@ -480,8 +480,8 @@ def run_e2e(args, dist: Dist, vs, n_local: int) -> dict:
     from paper_1804_10120_b200 import bench as tb
     from paper_1804_10120_b200.evaluator import plan_for
 
-    # pinned host slab: at most 2^25 points (17 GB for P2) per box
-    s = max(256, min(args.e2e_slab, n_local, (1 << 25) // dist.world))
+    # pinned host slab: at most 2^26 points (34 GB of P2 fields) per box
+    s = max(256, min(args.e2e_slab, n_local, (1 << 26) // dist.world))
     prog, _ = tb.load(tb.P2)
     host = tb.make_env(prog, "Gamma", s, SEED, device="cpu")
     for f in host.values():  # pinned host memory for full-speed async copies
