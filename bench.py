@@ -57,7 +57,7 @@ def parse_args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--points", type=int, default=C5_POINTS, help="total grid points")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--e2e-slab", type=int, default=1 << 25,
+    ap.add_argument("--e2e-slab", type=int, default=1 << 26,
                     help="points per pinned host slab of the e2e leg")
     ap.add_argument("--cpu-sample", type=int, default=1 << 22,
                     help="points of the CPU-baseline sample")

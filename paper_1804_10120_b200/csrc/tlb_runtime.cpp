@@ -14,15 +14,18 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <sys/stat.h>
@@ -83,6 +86,9 @@ struct Driver {
   CUresult (*MemHostRegister)(void*, size_t, unsigned) = nullptr;
   CUresult (*MemHostUnregister)(void*) = nullptr;
   CUresult (*PointerGetAttribute)(void*, CUpointer_attribute, CUdeviceptr) = nullptr;
+  CUresult (*MemHostAlloc)(void**, size_t, unsigned) = nullptr;
+  CUresult (*MemFreeHost)(void*) = nullptr;
+  CUresult (*EventSynchronize)(CUevent) = nullptr;
 };
 
 // NVRTC subset (the nvrtcProgram handle is an opaque pointer).
@@ -171,7 +177,10 @@ int load_driver_locked() {
             bind(h, g_cu.MemcpyDtoHAsync, "cuMemcpyDtoHAsync_v2") &&
             bind(h, g_cu.MemHostRegister, "cuMemHostRegister_v2") &&
             bind(h, g_cu.MemHostUnregister, "cuMemHostUnregister") &&
-            bind(h, g_cu.PointerGetAttribute, "cuPointerGetAttribute");
+            bind(h, g_cu.PointerGetAttribute, "cuPointerGetAttribute") &&
+            bind(h, g_cu.MemHostAlloc, "cuMemHostAlloc") &&
+            bind(h, g_cu.MemFreeHost, "cuMemFreeHost") &&
+            bind(h, g_cu.EventSynchronize, "cuEventSynchronize");
   if (!ok) return fail("tlb: libcuda.so.1 lacks a required symbol");
   CUresult r = g_cu.Init(0);
   if (r != CUDA_SUCCESS) return fail("tlb: cuInit failed (%d)", (int)r);
@@ -232,8 +241,95 @@ struct StageSet {
   CUstream side[kStageBuffers] = {};
   CUdeviceptr scratch = 0;
   size_t scratch_bytes = 0;
+  // pinned host bounce ring for PAGEABLE callers (kStageBuffers x m x slab
+  // doubles, kept across calls) and one completion event per buffer
+  void* hpin = nullptr;
+  size_t hpin_bytes = 0;
+  CUevent done[kStageBuffers] = {};
   bool busy = false;
 };
+
+// Host copy workers for the pageable bounce path: run(ntasks, fn) calls
+// fn(0..ntasks-1) across the pool and the calling thread, returning when
+// all are done.  One run at a time (a mutex), workers created on first use.
+class CopyPool {
+ public:
+  void run(long long ntasks, const std::function<void(long long)>& fn) {
+    std::lock_guard<std::mutex> one(run_mu_);
+    start();
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      ntasks_ = ntasks;
+      next_.store(0);
+      active_ = nworkers_;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return active_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void start() {
+    if (started_) return;
+    started_ = true;
+    int n = (int)std::thread::hardware_concurrency();
+    if (const char* e = getenv("TLB_COPY_THREADS")) n = atoi(e);
+    n = std::max(1, std::min(n, 32));
+    // detached: the pool lives for the process (never destroyed), so exit
+    // never waits on or tears down a worker
+    for (int i = 1; i < n; ++i) std::thread([this] { loop(); }).detach();
+    nworkers_ = n - 1;
+  }
+  void work() {
+    for (long long t; (t = next_.fetch_add(1)) < ntasks_;) (*fn_)(t);
+  }
+  void loop() {
+    unsigned long long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      work();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--active_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  int nworkers_ = 0;
+  const std::function<void(long long)>* fn_ = nullptr;
+  std::atomic<long long> next_{0};
+  long long ntasks_ = 0;
+  int active_ = 0;
+  unsigned long long gen_ = 0;
+  bool started_ = false;
+};
+CopyPool& g_copy_pool = *new CopyPool;  // intentionally never destroyed
+
+struct CopyTask {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+
+// memcpy of every task, split into <= 1 MiB pieces spread over the pool
+void parallel_copy(const std::vector<CopyTask>& tasks) {
+  constexpr size_t kPiece = 1 << 20;
+  std::vector<CopyTask> pieces;
+  for (const auto& t : tasks)
+    for (size_t off = 0; off < t.bytes; off += kPiece)
+      pieces.push_back({(char*)t.dst + off, (const char*)t.src + off,
+                        std::min(kPiece, t.bytes - off)});
+  g_copy_pool.run((long long)pieces.size(), [&](long long i) {
+    memcpy(pieces[i].dst, pieces[i].src, pieces[i].bytes);
+  });
+}
 
 struct CtxState {
   int sm_count = 0;
@@ -848,15 +944,31 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
   if (load_module(k, ctx, &L)) return 1;
   const size_t m = k->slot_field.size();
   const int nb = kStageBuffers;
+  // pageable host arrays (not cudaHostAlloc'd, not registered): unless the
+  // caller asks for registration, copy them through a pinned bounce ring with
+  // the host copy pool, overlapped with the DMA of the neighbouring slabs —
+  // instead of the driver's serial internal staging of pageable copies
+  bool bounce = false;
+  const bool do_register = host_register_enabled();
+  if (!do_register) {
+    for (size_t j = 0; j < m && !bounce; ++j) {
+      unsigned int mt = 0;
+      const double* p = comp_ptrs[k->slot_field[j]][k->slot_comp[j]];
+      bounce = g_cu.PointerGetAttribute(&mt, CU_POINTER_ATTRIBUTE_MEMORY_TYPE,
+                                        (CUdeviceptr)p) != CUDA_SUCCESS;
+    }
+  }
   if (slab <= 0) {
-    // nb buffers of m*slab doubles, at most ~4 GiB in total
-    long long cap = (4LL << 30) / (long long)(nb * m * sizeof(double));
-    slab = std::min<long long>(n, std::max<long long>(1 << 16, cap));
+    // nb buffers of m*slab doubles, at most ~4 GiB in total; bounced runs use
+    // ~64 MiB per buffer (the pinned ring is the same size on the host)
+    long long cap = (bounce ? (64LL << 20) * nb : (4LL << 30)) /
+                    (long long)(nb * m * sizeof(double));
+    slab = std::min<long long>(n, std::max<long long>(bounce ? 4096 : 1 << 16, cap));
   }
   slab = std::min(slab, n);
   slab = (slab + 255) / 256 * 256;  // keeps every slot slice 2 KiB aligned
   HostPins pins;
-  if (host_register_enabled()) {
+  if (do_register) {
     std::vector<std::pair<uintptr_t, uintptr_t>> spans;
     for (size_t j = 0; j < m; ++j) {
       const uintptr_t a = (uintptr_t)(comp_ptrs[k->slot_field[j]][k->slot_comp[j]]);
@@ -881,6 +993,18 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
   for (int s = 0; s < nb; ++s)
     if (!set->side[s])
       CU(g_cu.StreamCreate(&set->side[s], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+  if (bounce) {
+    if (set->hpin_bytes < need) {
+      if (set->hpin) g_cu.MemFreeHost(set->hpin);
+      set->hpin = nullptr;
+      set->hpin_bytes = 0;
+      CU(g_cu.MemHostAlloc(&set->hpin, need, CU_MEMHOSTALLOC_PORTABLE), "cuMemHostAlloc(bounce)");
+      set->hpin_bytes = need;
+    }
+    for (int s = 0; s < nb; ++s)
+      if (!set->done[s])
+        CU(g_cu.EventCreate(&set->done[s], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  }
   // order after prior work of the caller's stream
   CUevent ev;
   CU(g_cu.EventCreate(&ev, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
@@ -889,16 +1013,46 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
     CU(g_cu.StreamWaitEvent(set->side[s], ev, 0), "cuStreamWaitEvent");
   g_cu.EventDestroy(ev);
   std::vector<uint64_t> slots(m);
+  // bounce ring: buffer b holds slot j of its slab at hpin + (b*m + j)*slab
+  auto pinned = [&](int b, size_t j) {
+    return (double*)set->hpin + ((size_t)b * m + j) * (size_t)slab;
+  };
+  struct Pending {
+    long long lo = -1, cnt = 0;
+  } pend[kStageBuffers];
+  auto drain = [&](int b) -> int {  // outputs of buffer b's slab: pinned -> caller
+    if (pend[b].lo < 0) return 0;
+    CU(g_cu.EventSynchronize(set->done[b]), "cuEventSynchronize(bounce)");
+    std::vector<CopyTask> out;
+    for (size_t j = 0; j < m; ++j)
+      if (k->slot_flags[j] & TLB_SLOT_WRITE)
+        out.push_back({const_cast<double*>(comp_ptrs[k->slot_field[j]][k->slot_comp[j]]) +
+                           pend[b].lo,
+                       pinned(b, j), (size_t)pend[b].cnt * sizeof(double)});
+    parallel_copy(out);
+    pend[b].lo = -1;
+    return 0;
+  };
   long long slab_idx = 0;
   for (long long lo = 0; lo < n; lo += slab, ++slab_idx) {
     const long long cnt = std::min(slab, n - lo);
     const int b = (int)(slab_idx % nb);
     CUstream s = set->side[b];
     CUdeviceptr buf = set->scratch + (size_t)b * m * (size_t)slab * sizeof(double);
+    if (bounce) {
+      if (drain(b)) return 1;  // buffer b's previous slab (nb slabs ago) is done
+      std::vector<CopyTask> in;
+      for (size_t j = 0; j < m; ++j)
+        if (k->slot_flags[j] & TLB_SLOT_READ)
+          in.push_back({pinned(b, j), comp_ptrs[k->slot_field[j]][k->slot_comp[j]] + lo,
+                        (size_t)cnt * sizeof(double)});
+      parallel_copy(in);
+    }
     for (size_t j = 0; j < m; ++j) {
       slots[j] = buf + j * (size_t)slab * sizeof(double);
       if (k->slot_flags[j] & TLB_SLOT_READ) {
-        const double* src = comp_ptrs[k->slot_field[j]][k->slot_comp[j]] + lo;
+        const double* src =
+            bounce ? pinned(b, j) : comp_ptrs[k->slot_field[j]][k->slot_comp[j]] + lo;
         CU(g_cu.MemcpyHtoDAsync(slots[j], src, (size_t)cnt * sizeof(double), s), "H2D");
       }
     }
@@ -910,11 +1064,21 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
       return 1;
     for (size_t j = 0; j < m; ++j) {
       if (k->slot_flags[j] & TLB_SLOT_WRITE) {
-        double* dst = const_cast<double*>(comp_ptrs[k->slot_field[j]][k->slot_comp[j]]) + lo;
+        double* dst = bounce ? pinned(b, j)
+                             : const_cast<double*>(comp_ptrs[k->slot_field[j]][k->slot_comp[j]]) +
+                                   lo;
         CU(g_cu.MemcpyDtoHAsync(dst, slots[j], (size_t)cnt * sizeof(double), s), "D2H");
       }
     }
+    if (bounce) {
+      CU(g_cu.EventRecord(set->done[b], s), "cuEventRecord(bounce)");
+      pend[b].lo = lo;
+      pend[b].cnt = cnt;
+    }
   }
+  if (bounce)  // the last nb slabs, oldest first
+    for (long long i = std::max(0LL, slab_idx - nb); i < slab_idx; ++i)
+      if (drain((int)(i % nb))) return 1;
   for (int s = 0; s < nb; ++s)
     CU(g_cu.StreamSynchronize(set->side[s]), "cuStreamSynchronize");
   return 0;
@@ -933,10 +1097,13 @@ int tlb_release_staging(void) {
   }
   std::lock_guard<std::mutex> lk(st->stage_mu);
   for (auto& set : st->sets) {
-    if (set->busy || !set->scratch) continue;  // a running pipeline keeps its buffers
-    CU(g_cu.MemFree(set->scratch), "cuMemFree(staging)");
+    if (set->busy) continue;  // a running pipeline keeps its buffers
+    if (set->scratch) CU(g_cu.MemFree(set->scratch), "cuMemFree(staging)");
     set->scratch = 0;
     set->scratch_bytes = 0;
+    if (set->hpin) CU(g_cu.MemFreeHost(set->hpin), "cuMemFreeHost(bounce)");
+    set->hpin = nullptr;
+    set->hpin_bytes = 0;
   }
   return 0;
 }

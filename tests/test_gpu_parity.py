@@ -74,6 +74,27 @@ def test_host_fields_staged_through_gpu_bitwise(name):
     _check(case, env_to_host(env), want)
 
 
+@pytest.mark.parametrize("register", ["0", "1"])
+@pytest.mark.parametrize("name", ["p2", "p3"])
+def test_pageable_host_fields_through_the_bounce_ring(name, register, monkeypatch):
+    # pageable (numpy) host fields large enough for many bounce slabs: the
+    # pinned ring wraps several times, the last slab is ragged, and outputs
+    # drain oldest-first; TLB_HOST_REGISTER=1 takes the page-locking path
+    from paper_1804_10120_b200 import bench as tb
+
+    monkeypatch.setenv("TLB_HOST_REGISTER", register)
+    prog, vs = tb.load(tb.PROGRAMS[name])
+    n = 131072 * 7 + 333  # P2: 64 slots -> 131072-point bounce slabs
+    host = random_host_env(prog, n, 23)
+    want = {k: a.copy() for k, a in host.items()}
+    numpy_eval.eval_program(vs, want)
+    env = numpy_env(prog, host)
+    eval_program(vs, env)
+    got = env_to_host(env)
+    for k in want:
+        assert same_bits(got[k], want[k]), k
+
+
 @pytest.mark.parametrize("name", ["c1_dtg_odd", "c3_christoffel", "suite_contract3"])
 @pytest.mark.parametrize("chunk", [1, 7, 32])
 def test_chunking_is_invisible(name, chunk):
