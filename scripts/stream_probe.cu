@@ -201,6 +201,28 @@ __global__ void __launch_bounds__(256) probe_mix(const __grid_constant__ MixPtrs
   }
 }
 
+// the same mix, one point (8-byte accesses) per thread, the shape of the
+// policy-3 heavier kernels (tlk_flat_v1, 128-thread blocks)
+struct MixPtrs1 {
+  const double* r[64];
+  double* w[64];
+};
+template <int R, int W>
+__global__ void __launch_bounds__(256) probe_mix1(const __grid_constant__ MixPtrs1 P, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      double v;
+      asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(P.r[j] + i));
+      s += v;
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) __stcs(P.w[j] + i, s + j);
+  }
+}
+
 static int sms() {
   int d = 0, n = 0;
   cudaGetDevice(&d);
@@ -287,6 +309,20 @@ int sp_bulk(const void* a, long long bytes, int chunk, int blocks_per_sm, void* 
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 32768);
     k<<<g, 32, 6 * 32768, s>>>((const char*)a, bytes);
   }
+  return (int)cudaGetLastError();
+}
+// one point per thread; blocks_per_sm <= 0: one-shot grid (n / threads blocks)
+int sp_mix1(const void* const* r, int nr, void* const* w, int nw, long long n, int blocks_per_sm,
+            int threads, void* stream) {
+  MixPtrs1 P;
+  for (int j = 0; j < nr && j < 64; ++j) P.r[j] = (const double*)r[j];
+  for (int j = 0; j < nw && j < 64; ++j) P.w[j] = (double*)w[j];
+  long long g = blocks_per_sm > 0 ? (long long)sms() * blocks_per_sm : (n + threads - 1) / threads;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nr == 40 && nw == 24) probe_mix1<40, 24><<<(unsigned)g, threads, 0, s>>>(P, n);
+  else if (nr == 1 && nw == 1) probe_mix1<1, 1><<<(unsigned)g, threads, 0, s>>>(P, n);
+  else if (nr == 5 && nw == 3) probe_mix1<5, 3><<<(unsigned)g, threads, 0, s>>>(P, n);
+  else return -1;
   return (int)cudaGetLastError();
 }
 int sp_mix(const void* const* r, int nr, void* const* w, int nw, long long n2, int blocks_per_sm,

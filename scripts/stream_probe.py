@@ -113,6 +113,10 @@ def main():
             t = timeit(lambda: lib.sp_mix(rp, nr, wp, nw, ctypes.c_longlong(m // 2), bps, st))
             rec("mix_ldg128_stcs128", 8 * m * (nr + nw), t, reads=nr, writes=nw,
                 blocks_per_sm=bps)
+        for threads in (128, 256):
+            t = timeit(lambda: lib.sp_mix1(rp, nr, wp, nw, ctypes.c_longlong(m), 0, threads, st))
+            rec("mix_ldg64_stcs64_oneshot", 8 * m * (nr + nw), t, reads=nr, writes=nw,
+                threads=threads)
         del rs, ws
         torch.cuda.empty_cache()
     return res
