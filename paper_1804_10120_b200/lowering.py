@@ -642,14 +642,21 @@ def _policy3(reads: int, writes: int, n_ops: int, rw_slots: int, chained: int) -
     * heavier: 1 point per thread, 128-thread blocks (register-heavy
       bodies: finer block granularity — P2 +0.3-4 %, P3 +17-23 %, contract1
       +3-4 % over 256 threads);
-    * read-modify-write slots: as policy 2 (2 points per thread, 4 waves,
-      no restrict).
+    * read-modify-write slots (`op=` statements, or a program that writes a
+      field it also reads): 1 point per thread, 128-thread blocks, every
+      load hoisted, no restrict.
     Loads stay as fitted in round 1 (hoisted for light and chained programs,
     movable ld.global.nc for heavier read-only ones).  The TMA-staged entry
     remains available as a variant (``stage``), bit-exact and tested."""
     arrays = reads + writes
     if rw_slots:
-        return Variant(restrict=False, hoist=False, ldmode=0, vec=2, waves=4)
+        # every load hoisted (the loads are not movable: ld.global.cs beside
+        # stores of the same slots), one point per thread, 128-thread blocks:
+        # +7-40 % over policy 2's 2-point 4-wave grid at 2^26
+        # (profiles/r02/tuning/tune_ab_read_modify_write.jsonl: A+=B +9 %,
+        # A*=2 +9 %, Gamma+= +40 %, dtg+= +7 %)
+        return Variant(restrict=False, hoist=True, ldmode=0, vec=1, waves=0, threads=128,
+                       batch_threads=256, batch_bound=256)
     # the multi-domain batch entries are unchanged from policy 2 (256-thread
     # launch bounds; 256- / 128-thread blocks): the flat entries' block size
     # must not change their code (P2's batch entry compiled for 128-thread

@@ -55,7 +55,7 @@ def source(name: str) -> str:
 
 def run(case):
     name, n = case["program"], int(case["n"])
-    prog, vs = tb.load(source(name))
+    prog, vs = tb.load(case.get("source") or source(name))
     base = lower_program(vs)
     if case.get("staged_only") and not base.variant.stage:
         print(json.dumps({"program": name, "N": n, "skipped": "not staged by the policy",
@@ -177,6 +177,26 @@ def main():
                     v["staged_np1"] = {"__launch__": {"vec": 3, "max_blocks": "tiles1"}}
                     v["staged_np4"] = {"__launch__": {"vec": 3, "max_blocks": "tiles4"}}
                 cases.append({"program": nm, "n": n, "variants": v})
+    if os.environ.get("RMW"):  # read-modify-write programs: policy geometry vs one-shot shapes
+        sizes = [int(x) for x in os.environ["RMW"].split(",")]
+        srcs = {
+            "rmw_add": "tensor A dim 3 rank 2;\ntensor B dim 3 rank 2;\nA(i, j) += B(i, j);\n",
+            "rmw_scale": "tensor A dim 3 rank 2 sym(0,1);\nA(sym<0,1>, i, j) *= 2.0;\n",
+            "rmw_gamma": tb.CHRISTOFFEL.replace(") = 0.5*", ") += 0.5*"),
+            "rmw_dtg": tb.DTG.replace(") = -2*", ") += -2*"),
+        }
+        cases = []
+        for n in sizes:
+            for nm, src in srcs.items():
+                cases.append({"program": nm, "n": n, "source": src, "variants": {
+                    "policy": {},
+                    "v1_np_t512": {"vec": 1, "waves": 0, "threads": 512, "hoist": True},
+                    "v1_np_t128": {"vec": 1, "waves": 0, "threads": 128},
+                    "v1_np_t256": {"vec": 1, "waves": 0, "threads": 256},
+                    "v2_np_t256": {"vec": 2, "waves": 0, "threads": 256},
+                    "v1_np_t128_h1": {"vec": 1, "waves": 0, "threads": 128, "hoist": True},
+                    "v1_np_t256_h1": {"vec": 1, "waves": 0, "threads": 256, "hoist": True},
+                    "v2_np_t256_h1": {"vec": 2, "waves": 0, "threads": 256, "hoist": True}}})
     if os.environ.get("HEAVY"):  # policy-3 heavier kernels: load flavour, hoist, register cap
         sizes = [int(x) for x in os.environ["HEAVY"].split(",")]
         cases = []

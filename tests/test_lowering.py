@@ -215,10 +215,11 @@ def test_default_policy_is_one_shot_flat(name, vec, threads, hoist, ldmode):
     assert k.max_blocks == 1 << 62 and k.vec == 1 and k.small is None
 
 
-def test_read_modify_write_programs_keep_the_two_point_waves():
+def test_read_modify_write_programs_run_hoisted_one_shot():
     _, vs = program("tensor A dim 3 rank 1;\ntensor B dim 3 rank 1;\nA(i) += B(i);\n")
     var = lower_program(vs).variant
-    assert (var.vec, var.waves, var.restrict) == (2, 4, False)
+    assert (var.vec, var.waves, var.threads, var.restrict, var.hoist, var.ldmode) == \
+        (1, 0, 128, False, True, 0)
 
 
 def test_stage_refused_for_read_write_and_read_free_programs():
