@@ -1,6 +1,6 @@
 #!/bin/bash
 # One GPU session: tests, smoke, bench (both arms), ncu launch list + full capture.
-# Usage (under gpurun): bash scripts/gpu_session.sh [tag]
+# Usage (under gpurun): bash scripts/sessions/gpu_session.sh [tag]
 TAG=${1:-r01}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT

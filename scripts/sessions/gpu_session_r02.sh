@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-2 GPU session: parity suite, smoke, both bench arms, launch list and
-# one ncu --set full capture of the bench kernel.  Usage: OUT=gpurun_out/x bash scripts/gpu_session_r02.sh
+# one ncu --set full capture of the bench kernel.  Usage: OUT=gpurun_out/x bash scripts/sessions/gpu_session_r02.sh
 set -u
 OUT=${OUT:-gpurun_out/r02}
 mkdir -p "$OUT"

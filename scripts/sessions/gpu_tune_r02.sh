@@ -2,7 +2,7 @@
 # Round-2 tuning session: warp-specialised staged
 # entry parity, P2 knobs + streaming ceilings at 2^28, component-pitch
 # padding, C1 64^3 / C3 128^3 launch shapes.
-# Usage: OUT=gpurun_out/x bash scripts/gpu_tune_r02.sh
+# Usage: OUT=gpurun_out/x bash scripts/sessions/gpu_tune_r02.sh
 set -u
 OUT=${OUT:-gpurun_out/tune_r02}
 mkdir -p "$OUT"
