@@ -399,6 +399,44 @@ def test_concurrent_streams():
         _check(case, env_to_host(env), want)
 
 
+def test_concurrent_host_staged_runs_from_threads():
+    # several host threads each evaluate pageable (numpy) fields at once: the
+    # runs take their own staging sets (two per context; a third waits), share
+    # the host copy pool, and each result is bit-identical to the oracle
+    import threading
+
+    from paper_1804_10120_b200 import bench as tb
+
+    prog, vs = tb.load(tb.P2)
+    n = 131072 * 3 + 77
+    hosts = [random_host_env(prog, n, 100 + t) for t in range(3)]
+    wants = []
+    for h in hosts:
+        w = {k: a.copy() for k, a in h.items()}
+        numpy_eval.eval_program(vs, w)
+        wants.append(w)
+    envs = [numpy_env(prog, h) for h in hosts]
+    errors = []
+
+    def work(env):
+        try:
+            for _ in range(2):
+                eval_program(vs, env)
+        except Exception as exc:  # noqa: BLE001
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(e,)) for e in envs]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for env, w in zip(envs, wants):
+        got = env_to_host(env)
+        for k in ("Gamma", "dtg"):
+            assert same_bits(got[k], w[k]), k
+
+
 def test_foreign_ir_classes_are_accepted():
     # the evaluator reads IR by class *name* and attributes (SURVEY 8b
     # drop-in): a tree made of another package's classes — here stand-ins
