@@ -965,6 +965,9 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
                     (long long)(nb * m * sizeof(double));
     slab = std::min<long long>(n, std::max<long long>(bounce ? 4096 : 1 << 16, cap));
   }
+  if (bounce)  // an explicit slab too: the pinned ring stays ~64 MiB per buffer
+    slab = std::min<long long>(
+        slab, std::max<long long>(4096, (64LL << 20) / (long long)(m * sizeof(double))));
   slab = std::min(slab, n);
   slab = (slab + 255) / 256 * 256;  // keeps every slot slice 2 KiB aligned
   HostPins pins;
