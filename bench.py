@@ -692,7 +692,7 @@ def config_table(gpu_rows, cpu_rows, line, args) -> dict | None:
     g3 = lambda x: None if x is None else float(f"{x:.3g}")  # noqa: E731
     m3 = lambda x: None if x is None else float(f"{x / 1e6:.3g}")  # noqa: E731
     cols = ["N", "gpu_us", "gpu_frac", "gpu_Mpts_s", "cpu_c_Mpts_s", "cpu_np1_Mpts_s",
-            "cpu_npT_Mpts_s"]
+            "cpu_npT_Mpts_s", "gpu_us_b2b"]
     out: dict = {"cols": cols}
     keys = list((gpu_rows or {}).get("rows", {}).keys())
     for k in (cpu_rows or {}):
@@ -705,11 +705,11 @@ def config_table(gpu_rows, cpu_rows, line, args) -> dict | None:
         if k == "C5_p2_2^28":
             r = line["roofline"]
             g = {"N": args.points, "us": line["ms_per_step"] * 1e3, "frac": r["frac"],
-                 "pts": line["value"]}
+                 "pts": line["value"], "us_b2b": line["ms_per_step"] * 1e3}
             cb = line.get("cpu_baseline") or {}
             c = {"c": cb.get("value")}
         row = [g.get("N", _n_of(k)), g3(g.get("us")), g3(g.get("frac")), m3(g.get("pts")),
-               m3(c.get("c")), m3(c.get("np1")), m3(c.get("npT"))]
+               m3(c.get("c")), m3(c.get("np1")), m3(c.get("npT")), g3(g.get("us_b2b"))]
         out[k] = row
     if cpu_rows:
         out["cpu_host"] = cpu_rows.get("host")
@@ -854,7 +854,9 @@ def run_configs() -> dict:
                        "L2 flush (256 MB write + 256 MB read: cold, clean L2), CUDA events; C4 "
                        "= one batched launch for all 512 subdomains; gpu_frac: algorithmic "
                        "bytes / time / MEASURED_PEAKS hbm_gbs; floor_us: same for a 1-element "
-                       "kernel (event + launch overhead included in every gpu_us)")}
+                       "kernel (event + launch overhead included in every gpu_us); gpu_us_b2b: "
+                       "per launch over 20 back-to-back launches in one CUDA graph (steady "
+                       "state; working sets under the 126 MB L2 are re-read from it)")}
 
 
 def run_reference(args, dist: Dist) -> dict | None:

@@ -42,7 +42,8 @@ def test_config_table_is_compact_and_last():
     sys.path.insert(0, str(ROOT))
     import bench
 
-    gpu = {"rows": {"C1_dtg_64^3": {"N": 64**3, "us": 8.1, "frac": 0.87, "pts": 3.2e10}},
+    gpu = {"rows": {"C1_dtg_64^3": {"N": 64**3, "us": 8.1, "frac": 0.87, "pts": 3.2e10,
+                                    "us_b2b": 6.4}},
            "floor_us": 2.0, "method": "m"}
     cpu = {"C1_dtg_64^3": {"c": 2.7e8, "c_n": 64**3, "np1": 2.2e7, "np_n": 64**3, "npT": 1e7},
            "host": "16x cpu"}
@@ -53,8 +54,10 @@ def test_config_table_is_compact_and_last():
         points = 1 << 28
 
     t = bench.config_table(gpu, cpu, line, A)
-    assert t["C1_dtg_64^3"] == [262144, 8.1, 0.87, 32000.0, 270.0, 22.0, 10.0]
+    assert t["C1_dtg_64^3"] == [262144, 8.1, 0.87, 32000.0, 270.0, 22.0, 10.0, 6.4]
+    assert t["cols"][-1] == "gpu_us_b2b"
     assert t["C5_p2_2^28"][:2] == [1 << 28, 20500.0] and t["cpu_host"] == "16x cpu"
+    assert t["C5_p2_2^28"][-1] == 20500.0
     assert len(json.dumps(t)) < 2500
 
 
