@@ -907,6 +907,13 @@ int tlb_batch_launch(tlb_batch* b, int vec, int threads, void* stream) {
     long long cap = (long long)st->sm_count * L->occ[e] * waves;
     if (gx * gy > cap) gx = std::max(1LL, cap / gy);
   }
+  // tuning knob (TLB_BATCH_CHUNKS=c): c chunks of a domain per block, so a
+  // block stages the domain's slot pointers once per c x threads points
+  static const long long chunks = [] {
+    const char* e = getenv("TLB_BATCH_CHUNKS");
+    return e ? std::max(1LL, atoll(e)) : 1LL;
+  }();
+  if (chunks > 1) gx = std::max(1LL, (gx + chunks - 1) / chunks);
   CUdeviceptr table = b->table;
   int ndom = b->ndom;
   void* args[] = {&table, &ndom};
