@@ -169,7 +169,7 @@ struct tlk_shared_ptrs {
 };
 
 extern "C" __global__ void __launch_bounds__(TLK_THREADS, TLK_MINB)
-tlk_flat_v1(const tlk_flat_params prm) {
+tlk_flat_v1(const __grid_constant__ tlk_flat_params prm) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   TLK_LOOP
   for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < prm.n; x += stride)
@@ -177,7 +177,7 @@ tlk_flat_v1(const tlk_flat_params prm) {
 }
 
 extern "C" __global__ void __launch_bounds__(TLK_THREADS, TLK_MINB)
-tlk_flat_v2(const tlk_flat_params prm) {
+tlk_flat_v2(const __grid_constant__ tlk_flat_params prm) {
   const long long pairs = prm.n >> 1;
   const long long stride = (long long)gridDim.x * blockDim.x;
   TLK_LOOP

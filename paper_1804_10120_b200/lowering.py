@@ -194,6 +194,7 @@ class _Builder:
         self.shadow: dict[int, Any] = {}  # slot -> current operand
         self.flops = 0
         self.chained = 0  # reads served by the register shadow of a written slot
+        self.groups = 1  # output groups (Variant.vn = 1: one device function each)
 
     def slot(self, f: int, c: int) -> int:
         key = (f, c)
@@ -216,6 +217,26 @@ class _Builder:
             self.slot_flags[s] |= SLOT_READ
             self.shadow[s] = r
         return self.shadow[s]
+
+    def begin_group(self) -> None:
+        """Start a new output group (Variant.vn = 1): its instructions become
+        a separate non-inlined device function, so nothing — loaded inputs,
+        shared subexpressions — stays live from one group into the next, and
+        the compiler cannot merge a group's recomputed subexpressions with an
+        earlier group's.  Only for programs whose outputs never read a
+        written slot (the register shadow then holds loads only)."""
+        self.instrs.append(Instr("grp"))
+        self.groups += 1
+        self.vn.clear()
+        self.shadow.clear()
+
+    def snapshot(self):
+        return len(self.instrs), dict(self.vn), dict(self.shadow), self.flops
+
+    def rollback(self, snap) -> None:
+        n, vn, shadow, flops = snap
+        del self.instrs[n:]
+        self.vn, self.shadow, self.flops = vn, shadow, flops
 
     def write(self, f: int, c: int, val) -> None:
         s = self.slot(f, c)
@@ -344,22 +365,38 @@ class _Lowerer:
             return acc
         raise LoweringError(f"not an expression node: {e!r}")
 
-    def statement(self, v, only: set[int] | None = None) -> None:
+    def statement(self, v, only: set[int] | None = None, budget: int = 0) -> None:
+        """Lower one statement, its canonical LHS components in storage order.
+        ``budget`` > 0 splits the outputs into groups (Builder.begin_group)
+        whose bodies keep at most ~budget values live (_max_live): an output
+        that would push the current group past it starts the next group."""
         stmt = v.stmt
-        lhs = stmt.lhs
         dims = tuple(var.dim for var in v.lhs_vars)
         for n, values in enumerate(iter_canonical(dims, as_sym(v.loop_sym))):
             if only is not None and n not in only:
                 continue
             binding = dict(zip(v.lhs_vars, values))
-            f, c = self.leaf_slot(v, lhs, binding)
-            rhs = self.expr(v, stmt.rhs, binding)
-            if stmt.op == "=":
-                val = rhs
-            else:
-                cur = self.b.read(f, c)
-                val = self.b.binary(_AUG[stmt.op], cur, rhs)
-            self.b.write(f, c, val)
+            snap = self.b.snapshot() if budget else None
+            self.component(v, binding)
+            if budget:
+                start = max((k for k, i in enumerate(self.b.instrs[:snap[0]]) if i.op == "grp"),
+                            default=-1) + 1
+                had_output = any(i.op == "st" for i in self.b.instrs[start:snap[0]])
+                if had_output and _max_live(self.b.instrs[start:]) > budget:
+                    self.b.rollback(snap)
+                    self.b.begin_group()
+                    self.component(v, binding)
+
+    def component(self, v, binding) -> None:
+        stmt = v.stmt
+        f, c = self.leaf_slot(v, stmt.lhs, binding)
+        rhs = self.expr(v, stmt.rhs, binding)
+        if stmt.op == "=":
+            val = rhs
+        else:
+            cur = self.b.read(f, c)
+            val = self.b.binary(_AUG[stmt.op], cur, rhs)
+        self.b.write(f, c, val)
 
 
 _AUG = {"+=": "add", "-=": "sub", "*=": "mul", "/=": "div"}
@@ -385,6 +422,8 @@ def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = F
     slot, and none is asked to.  ``hoist_loads`` additionally places all
     loads first in the source.
     """
+    if any(ins.op == "grp" for ins in instrs):
+        return _emit_groups(instrs, slot_flags, hoist_loads, restrict, direct)
     # keep only the final store of every slot; earlier values were consumed
     # through the register shadow
     last = {}
@@ -438,6 +477,68 @@ def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = F
     return out
 
 
+def _emit_instr(ins: Instr, ptr, direct, keep_store: bool) -> str | None:
+    if ins.op == "ld":
+        ld = "(LD == 3 ? 1 : LD)" if ins.slot in direct else "LD"
+        return f"  const T v{ins.dst} = tl_ld<T, {ld}>({ptr(ins.slot)} + x);"
+    if ins.op == "st":
+        if not keep_store:
+            return None
+        val = ins.a
+        src = f"tl_splat<T>{val.c_text()}" if isinstance(val, _Lit) else f"v{val}"
+        return f"  tl_st({ptr(ins.slot)} + x, {src});"
+    if ins.op in _CSYM:
+        return f"  const T v{ins.dst} = {_operand(ins.a)} {_CSYM[ins.op]} {_operand(ins.b)};"
+    if ins.op == "neg":
+        return f"  const T v{ins.dst} = -{_operand(ins.a)};"
+    if ins.op == "sqrt":
+        return f"  const T v{ins.dst} = tl_sqrt({_operand(ins.a)});"
+    raise LoweringError(f"bad instruction {ins}")  # pragma: no cover
+
+
+def _emit_groups(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool,
+                 restrict: bool, direct) -> list[str]:
+    """Body of a program lowered in output groups (Variant.vn = 1): one
+    ``__noinline__`` device function per group, each loading what it reads
+    (through the kernel's parameter block, passed by reference:
+    ``__grid_constant__`` in the flat entries, so no copy), computing with its
+    own value numbering and storing its outputs; ``tlk_point`` calls them in
+    order.  Separate functions are what keeps ptxas from re-merging the
+    subexpressions groups recompute (its CSE sees through any inline asm)."""
+    last = {ins.slot: k for k, ins in enumerate(instrs) if ins.op == "st"}
+    groups: list[list[tuple[int, Instr]]] = [[]]
+    for k, ins in enumerate(instrs):
+        if ins.op == "grp":
+            groups.append([])
+        else:
+            groups[-1].append((k, ins))
+    out: list[str] = []
+    for g, items in enumerate(groups):
+        used = sorted({ins.slot for _, ins in items if ins.op in ("ld", "st")})
+        out += ["template <typename T, int LD, typename P>",
+                f"__device__ __noinline__ void tlk_grp{g}(const P& P_, const long long x) {{"]
+        if restrict:
+            for j in used:
+                q = "double* __restrict__" if slot_flags[j] & SLOT_WRITE else \
+                    "const double* __restrict__"
+                out.append(f"  {q} p{j} = P_.p[{j}];")
+            ptr = "p{}".format
+        else:
+            ptr = "P_.p[{}]".format
+        if hoist_loads:
+            items = [t for t in items if t[1].op == "ld"] + [t for t in items if t[1].op != "ld"]
+        for k, ins in items:
+            line = _emit_instr(ins, ptr, direct, last.get(ins.slot) == k)
+            if line is not None:
+                out.append(line)
+        out.append("}")
+    out += ["template <typename T, int LD = TLK_LDMODE, typename P>",
+            "__device__ __forceinline__ void tlk_point(const P& P_, const long long x) {"]
+    out += [f"  tlk_grp{g}<T, LD>(P_, x);" for g in range(len(groups))]
+    out.append("}")
+    return out
+
+
 _TEMPLATE_CACHE: list[str] = []
 
 
@@ -480,6 +581,7 @@ class Variant:
     minb: int = 0  # TLK_MINB: min resident blocks/SM of the flat entries (0 = unconstrained)
     stage_ws: int = 0  # TLK_STAGE_WS: staged entry with a dedicated producer warp (1) or not (0)
     batch_bound: int = 0  # TLK_BATCH_BOUND: the batch entries' __launch_bounds__ (0 = threads)
+    vn: int = 0  # 1: outputs split into groups, one non-inlined device function each
 
     def tag(self) -> str:
         t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
@@ -491,6 +593,7 @@ class Variant:
         t += f"m{self.minb}" if self.minb else ""
         t += "p" if self.stage and self.stage_ws else ""
         t += f"q{self.batch_bound}" if self.batch_bound else ""
+        t += "u" if self.vn else ""
         return t + (f"n{self.threads}" if self.threads != 256 else "")
 
     def small_class(self) -> "Variant":
@@ -517,10 +620,10 @@ class Variant:
         launch-time choices; both entry points are in every module)."""
         return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs, self.stage,
                  self.threads, self.stage_threads, self.stage_reads, self.minb, self.stage_ws,
-                 self.batch_bound)
+                 self.batch_bound, self.vn)
                 == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs, other.stage,
                     other.threads, other.stage_threads, other.stage_reads, other.minb,
-                    other.stage_ws, other.batch_bound))
+                    other.stage_ws, other.batch_bound, other.vn))
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -745,11 +848,19 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     then TLK_* environment overrides)."""
     if not statements:
         raise LoweringError("nothing to lower: no statements")
-    low = _Lowerer(alias)
-    lhs_fields = []
-    for k, v in enumerate(statements):
-        lhs_fields.append(low.tensor(v, v.stmt.lhs.field))
-        low.statement(v, None if components is None else components[k])
+
+    def lower(budget: int):
+        low = _Lowerer(alias)
+        lhs = []
+        for k, v in enumerate(statements):
+            lhs.append(low.tensor(v, v.stmt.lhs.field))
+            low.statement(v, None if components is None else components[k], budget)
+        return low, lhs
+
+    low, lhs_fields = lower(0)
+    if variant is not None and variant.vn and not low.b.chained and not any(
+            f == SLOT_READ | SLOT_WRITE for f in low.b.slot_flags):
+        low, lhs_fields = lower(VN_LIVE_BUDGET)
     b = low.b
     n_slots = len(b.slots)
     if n_slots > MAX_PARAM_SLOTS:
@@ -761,7 +872,7 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     slot_comp = [0] * n_slots
     for (f, c), s in b.slots.items():
         slot_field[s], slot_comp[s] = f, c
-    n_ops = sum(1 for i in b.instrs if i.op not in ("ld", "st"))
+    n_ops = sum(1 for i in b.instrs if i.op not in ("ld", "st", "grp"))
     reads = sum(1 for f in b.slot_flags if f & SLOT_READ)
     writes = sum(1 for f in b.slot_flags if f & SLOT_WRITE)
     rw = sum(1 for f in b.slot_flags if f == SLOT_READ | SLOT_WRITE)
@@ -774,6 +885,18 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
             frac = float(os.environ["TLK_STAGE_FRAC"])
             variant = Variant(**{**variant.__dict__,
                                  "stage_reads": max(1, round(frac * reads))})
+        if _max_live(b.instrs) > VN_LIVE_BUDGET and not rw and not b.chained:
+            # program-wide value numbering keeps more values live than the
+            # register file holds (contract3: 761 doubles — 729 products
+            # shared across outputs — 5.7 KB of spills per thread): split the
+            # outputs into groups of at most ~VN_LIVE_BUDGET live values, one
+            # non-inlined device function each, recomputing what groups share
+            # (every output's own operation sequence is unchanged: same bits)
+            low2, lhs2 = lower(VN_LIVE_BUDGET)
+            if low2.b.groups > 1:
+                low, lhs_fields, b = low2, lhs2, low2.b
+                variant = Variant(**{**variant.__dict__, "vn": 1})
+                n_ops = sum(1 for i in b.instrs if i.op not in ("ld", "st", "grp"))
     if hoist_loads is not None:
         variant = Variant(**{**variant.__dict__, "hoist": hoist_loads})
     if variant.ldmode == 1 and rw:
@@ -854,6 +977,36 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     ident = f"{src}\0{slot_field}\0{slot_comp}\0{plan.slot_flags}\0{variant.tag()}"
     plan.key = hashlib.sha256(ident.encode()).hexdigest()
     return plan
+
+
+# largest number of simultaneously live values (doubles) program-wide value
+# numbering may leave in a kernel before the lowering splits the outputs into
+# groups (Variant.vn): 64 doubles = 128 registers leaves ptxas room for
+# addresses and the call ABI (48 / 64: no spills in contract2/3; 96: 56 / 248
+# bytes of spill stores; TLK_VN_BUDGET overrides, for tuning)
+VN_LIVE_BUDGET = int(os.environ.get("TLK_VN_BUDGET", "64"))
+
+
+def _max_live(instrs: list[Instr]) -> int:
+    """Peak number of simultaneously live SSA values when the body runs in
+    source order (a value lives from its definition to its last use) — the
+    register pressure the source order implies."""
+    last: dict[int, int] = {}
+    for k, ins in enumerate(instrs):
+        for o in (ins.a, ins.b):
+            if isinstance(o, int):
+                last[o] = k
+    live = peak = 0
+    for k, ins in enumerate(instrs):
+        if ins.op != "st" and ins.dst >= 0:
+            live += 1
+            peak = max(peak, live)
+            if ins.dst not in last:  # never used
+                live -= 1
+        for o in {ins.a, ins.b}:
+            if isinstance(o, int) and last.get(o) == k:
+                live -= 1
+    return peak
 
 
 def _phases(instrs: list[Instr]) -> int:

@@ -74,14 +74,25 @@ def run(case):
     kerns, plans, same, launch_kw = {}, {}, {}, {}
     want = None
     for label, over in case["variants"].items():
-        if "__policy__" in over:  # the lowering policy's own choice under TLK_POLICY=k
-            old = os.environ.get("TLK_POLICY")
-            os.environ["TLK_POLICY"] = str(over["__policy__"])
+        if "__policy__" in over or "__env__" in over:
+            # the lowering policy's own choice under TLK_POLICY=k / other env
+            envs = dict(over.get("__env__", {}))
+            if "__policy__" in over:
+                envs["TLK_POLICY"] = str(over["__policy__"])
+            saved = {k: os.environ.get(k) for k in envs}
+            os.environ.update(envs)
+            import importlib
+
+            from paper_1804_10120_b200 import lowering as _lw
+            _lw.VN_LIVE_BUDGET = int(os.environ.get("TLK_VN_BUDGET", "64"))
             plan = lower_program(vs)
-            if old is None:
-                os.environ.pop("TLK_POLICY")
-            else:
-                os.environ["TLK_POLICY"] = old
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k)
+                else:
+                    os.environ[k] = v
+            _lw.VN_LIVE_BUDGET = int(os.environ.get("TLK_VN_BUDGET", "64"))
+            del importlib
         else:
             var = Variant(**{**base.variant.__dict__,
                              **{k: v for k, v in over.items() if not k.startswith("__")}})
@@ -177,6 +188,15 @@ def main():
                     v["staged_np1"] = {"__launch__": {"vec": 3, "max_blocks": "tiles1"}}
                     v["staged_np4"] = {"__launch__": {"vec": 3, "max_blocks": "tiles4"}}
                 cases.append({"program": nm, "n": n, "variants": v})
+    if os.environ.get("GROUPS"):  # output groups (Variant.vn) for the contractions
+        sizes = [int(x) for x in os.environ["GROUPS"].split(",")]
+        cases = [{"program": nm, "n": n, "variants": {
+            "ungrouped": {"vn": 0},
+            "budget48": {"__env__": {"TLK_VN_BUDGET": "48"}},
+            "budget64": {"__env__": {"TLK_VN_BUDGET": "64"}},
+            "budget96": {"__env__": {"TLK_VN_BUDGET": "96"}},
+            "budget128": {"__env__": {"TLK_VN_BUDGET": "128"}}}}
+            for n in sizes for nm in ("contract2", "contract3")]
     if os.environ.get("RMW"):  # read-modify-write programs: policy geometry vs one-shot shapes
         sizes = [int(x) for x in os.environ["RMW"].split(",")]
         srcs = {

@@ -359,6 +359,40 @@ def test_every_codegen_variant_is_bit_exact(name, vkw):
     _check(case, env_to_host(env), want)
 
 
+@pytest.mark.parametrize("budget", [4, 16])
+@pytest.mark.parametrize("name", CASES)
+def test_output_groups_are_bit_exact(name, budget, monkeypatch):
+    # Variant.vn = 1: outputs split into groups of at most `budget` live
+    # values, one non-inlined device function each (the contractions' cure
+    # for spills) — forced here with tiny budgets on every golden program
+    # whose outputs never read a written slot
+    from paper_1804_10120_b200 import lowering
+    from paper_1804_10120_b200.evaluator import _bind, _fusion_plan
+    from paper_1804_10120_b200.runtime import Kernel
+
+    case = manifest()["cases"][name]
+    prog, vs = program(case["source"])
+    host, want = golden_io(name)
+    env = device_env(prog, host)
+    fp = _fusion_plan(vs, env)
+    if fp is None or case.get("raises"):
+        pytest.skip("program does not run as one fused launch")
+    monkeypatch.setattr(lowering, "VN_LIVE_BUDGET", budget)
+    plan = lowering.lower_program(vs, variant=lowering.Variant(vec=1, waves=0, threads=128,
+                                                               ldmode=1, vn=1))
+    if plan.variant.ldmode != 1 or "tlk_grp1" not in plan.source:
+        pytest.skip("read-modify-write or chained program, or a single group")
+    n, resizes = fp
+    for lhs, size in resizes:
+        lhs.resize(size)
+    _, _, stores = _bind(vs, env)
+    k = Kernel(plan)
+    for vec in (1, 2):
+        k.launch(n, [s_.base for s_ in stores], [s_.pitch for s_ in stores],
+                 torch.cuda.current_stream().cuda_stream, vec=vec if n % 2 == 0 else 1)
+        _check(case, env_to_host(env), want)
+
+
 def test_ragged_multi_domain_batch():
     # subdomains of different (odd and even) sizes in one launch
     prog, vs = program(manifest()["cases"]["c4_p2"]["source"])
