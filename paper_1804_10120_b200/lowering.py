@@ -885,7 +885,7 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
             frac = float(os.environ["TLK_STAGE_FRAC"])
             variant = Variant(**{**variant.__dict__,
                                  "stage_reads": max(1, round(frac * reads))})
-        if _max_live(b.instrs) > VN_LIVE_BUDGET and not rw and not b.chained:
+        if _max_live(b.instrs) > VN_LIVE_TRIGGER and not rw and not b.chained:
             # program-wide value numbering keeps more values live than the
             # register file holds (contract3: 761 doubles — 729 products
             # shared across outputs — 5.7 KB of spills per thread): split the
@@ -985,6 +985,12 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
 # addresses and the call ABI (48 / 64: no spills in contract2/3; 96: 56 / 248
 # bytes of spill stores; TLK_VN_BUDGET overrides, for tuning)
 VN_LIVE_BUDGET = int(os.environ.get("TLK_VN_BUDGET", "64"))
+# ... applied only when program-wide value numbering would keep more than this
+# many values live: grouping costs recomputation, which pays where the
+# ungrouped kernel spills heavily (contract3, 761 live: 58.4 -> 8.9 ms at
+# 2^24) but not where it barely spills (contract2, 94 live, 56 B of stack:
+# 5.08 -> 6.37 ms grouped; profiles/r02/tuning/tune_ab_output_groups.jsonl)
+VN_LIVE_TRIGGER = 128
 
 
 def _max_live(instrs: list[Instr]) -> int:
@@ -998,13 +1004,13 @@ def _max_live(instrs: list[Instr]) -> int:
                 last[o] = k
     live = peak = 0
     for k, ins in enumerate(instrs):
-        if ins.op != "st" and ins.dst >= 0:
+        for o in {ins.a, ins.b}:  # operands read at their last use die first
+            if isinstance(o, int) and last.get(o) == k:
+                live -= 1
+        if ins.op not in ("st", "grp") and ins.dst >= 0:
             live += 1
             peak = max(peak, live)
             if ins.dst not in last:  # never used
-                live -= 1
-        for o in {ins.a, ins.b}:
-            if isinstance(o, int) and last.get(o) == k:
                 live -= 1
     return peak
 

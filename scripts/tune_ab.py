@@ -188,8 +188,8 @@ def main():
                     v["staged_np1"] = {"__launch__": {"vec": 3, "max_blocks": "tiles1"}}
                     v["staged_np4"] = {"__launch__": {"vec": 3, "max_blocks": "tiles4"}}
                 cases.append({"program": nm, "n": n, "variants": v})
-    if os.environ.get("GROUPS"):  # output groups (Variant.vn) for the contractions
-        sizes = [int(x) for x in os.environ["GROUPS"].split(",")]
+    if os.environ.get("VNGROUPS"):  # output groups (Variant.vn) for the contractions
+        sizes = [int(x) for x in os.environ["VNGROUPS"].split(",")]
         cases = [{"program": nm, "n": n, "variants": {
             "ungrouped": {"vn": 0},
             "budget48": {"__env__": {"TLK_VN_BUDGET": "48"}},
