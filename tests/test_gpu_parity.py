@@ -393,6 +393,26 @@ def test_output_groups_are_bit_exact(name, budget, monkeypatch):
         _check(case, env_to_host(env), want)
 
 
+def test_grouped_program_in_a_multi_domain_batch():
+    # contract3 lowers in output groups; its batch entry calls the same
+    # group functions with the domain's slot pointers staged in shared memory
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.evaluator import kernel_for
+
+    src = {e.name: e.source for e in tb.builtin_suite()}["contract3"]
+    prog, vs = program(src)
+    hosts = [random_host_env(prog, n, 40 + n) for n in (4096, 1001, 4098)]
+    envs = [device_env(prog, h) for h in hosts]
+    assert kernel_for(vs, envs[0]).plan.variant.vn == 1
+    eval_batch(vs, envs)
+    for env, h in zip(envs, hosts):
+        want = {k: a.copy() for k, a in h.items()}
+        numpy_eval.eval_program(vs, want)
+        got = env_to_host(env)
+        for k in want:
+            assert same_bits(got[k], want[k]), k
+
+
 def test_ragged_multi_domain_batch():
     # subdomains of different (odd and even) sizes in one launch
     prog, vs = program(manifest()["cases"]["c4_p2"]["source"])
