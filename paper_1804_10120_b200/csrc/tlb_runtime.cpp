@@ -274,8 +274,11 @@ class CopyPool {
 
  private:
   void start() {
-    if (started_) return;
+    // a forked child inherits the pool's state but none of its threads:
+    // start its own
+    if (started_ && pid_ == getpid()) return;
     started_ = true;
+    pid_ = getpid();
     int n = (int)std::thread::hardware_concurrency();
     if (const char* e = getenv("TLB_COPY_THREADS")) n = atoi(e);
     n = std::max(1, std::min(n, 32));
@@ -309,6 +312,7 @@ class CopyPool {
   int active_ = 0;
   unsigned long long gen_ = 0;
   bool started_ = false;
+  pid_t pid_ = 0;
 };
 CopyPool& g_copy_pool = *new CopyPool;  // intentionally never destroyed
 
