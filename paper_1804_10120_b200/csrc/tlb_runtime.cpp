@@ -456,6 +456,7 @@ struct tlb_kernel {
   int dflt_waves = 1;
   int dflt_vec = 2;
   int batch_bound = 256;  // TLK_BATCH_BOUND: the batch entries' largest block
+  int chunk = 1;          // TLK_CHUNK: block-sized runs per block in tlk_flat_v1
   int stage_smem = 0;     // its dynamic shared memory (from the source)
   int stage_batch_smem = 0;  // tlk_stage_batch_v1's: the ring + NSTAGE x NSLOTS pointers
   std::mutex mu;
@@ -608,6 +609,7 @@ int tlb_compile(const char* src, const char* const* opts, int nopts, const char*
   // tile ring (TLK_NSTAGE x TLK_NREAD x TLK_THREADS doubles)
   k->threads = (int)source_define(src, "TLK_THREADS", 256);
   k->batch_bound = (int)source_define(src, "TLK_BATCH_BOUND", k->threads);
+  k->chunk = (int)std::max(1LL, source_define(src, "TLK_CHUNK", 1));
   k->dflt_waves = (int)source_define(src, "TLK_GRID_WAVES", 1);
   k->dflt_vec = (int)source_define(src, "TLK_VEC", 2) == 1 ? 1 : 2;
   const long long nstage = source_define(src, "TLK_NSTAGE", 0);
@@ -765,6 +767,7 @@ int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n, const uint6
     threads = (int)std::max(64LL, std::min<long long>(threads, (per + 31) / 32 * 32));
   }
   long long blocks = (units + threads - 1) / threads;
+  if (!vec2 && k->chunk > 1) blocks = (blocks + k->chunk - 1) / k->chunk;
   // max_blocks > 0: explicit cap; 0: one full wave at occupancy; -w: w waves
   int occ = L->occ[e];
   if (threads != k->threads) {

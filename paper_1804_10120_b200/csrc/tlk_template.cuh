@@ -168,12 +168,30 @@ struct tlk_shared_ptrs {
   double* const* p;
 };
 
+// TLK_CHUNK > 1 (tuning): a block takes TLK_CHUNK consecutive block-sized
+// runs of points before the grid strides on (one-shot grids then have
+// n / (threads * TLK_CHUNK) blocks; the runtime reads TLK_CHUNK from the source)
+#ifndef TLK_CHUNK
+#define TLK_CHUNK 1
+#endif
 extern "C" __global__ void __launch_bounds__(TLK_THREADS, TLK_MINB)
 tlk_flat_v1(const __grid_constant__ tlk_flat_params prm) {
+#if TLK_CHUNK > 1
+  const long long bstride = (long long)gridDim.x * blockDim.x * TLK_CHUNK;
+  for (long long base = (long long)blockIdx.x * blockDim.x * TLK_CHUNK; base < prm.n;
+       base += bstride) {
+#pragma unroll 1
+    for (int k = 0; k < TLK_CHUNK; ++k) {
+      const long long x = base + (long long)k * blockDim.x + threadIdx.x;
+      if (x < prm.n) tlk_point<double>(prm, x);
+    }
+  }
+#else
   const long long stride = (long long)gridDim.x * blockDim.x;
   TLK_LOOP
   for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < prm.n; x += stride)
     tlk_point<double>(prm, x);
+#endif
 }
 
 extern "C" __global__ void __launch_bounds__(TLK_THREADS, TLK_MINB)

@@ -582,6 +582,7 @@ class Variant:
     stage_ws: int = 0  # TLK_STAGE_WS: staged entry with a dedicated producer warp (1) or not (0)
     batch_bound: int = 0  # TLK_BATCH_BOUND: the batch entries' __launch_bounds__ (0 = threads)
     vn: int = 0  # 1: outputs split into groups, one non-inlined device function each
+    chunk: int = 1  # TLK_CHUNK: block-sized runs of points per block (tlk_flat_v1; tuning)
 
     def tag(self) -> str:
         t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
@@ -594,6 +595,7 @@ class Variant:
         t += "p" if self.stage and self.stage_ws else ""
         t += f"q{self.batch_bound}" if self.batch_bound else ""
         t += "u" if self.vn else ""
+        t += f"c{self.chunk}" if self.chunk > 1 else ""
         return t + (f"n{self.threads}" if self.threads != 256 else "")
 
     def small_class(self) -> "Variant":
@@ -620,10 +622,10 @@ class Variant:
         launch-time choices; both entry points are in every module)."""
         return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs, self.stage,
                  self.threads, self.stage_threads, self.stage_reads, self.minb, self.stage_ws,
-                 self.batch_bound, self.vn)
+                 self.batch_bound, self.vn, self.chunk)
                 == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs, other.stage,
                     other.threads, other.stage_threads, other.stage_reads, other.minb,
-                    other.stage_ws, other.batch_bound, other.vn))
+                    other.stage_ws, other.batch_bound, other.vn, other.chunk))
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -951,6 +953,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         header.append(f"#define TLK_MINB {variant.minb}")
     if variant.batch_bound:
         header.append(f"#define TLK_BATCH_BOUND {variant.batch_bound}")
+    if variant.chunk > 1:
+        header.append(f"#define TLK_CHUNK {variant.chunk}")
     if variant.stage:
         header.append(f"#define TLK_NSTAGE {variant.stage}")
         header.append(f"#define TLK_NREAD {len(rord) - rord.count(-1)}")

@@ -188,6 +188,13 @@ def main():
                     v["staged_np1"] = {"__launch__": {"vec": 3, "max_blocks": "tiles1"}}
                     v["staged_np4"] = {"__launch__": {"vec": 3, "max_blocks": "tiles4"}}
                 cases.append({"program": nm, "n": n, "variants": v})
+    if os.environ.get("CHUNKS"):  # block-local chunks in one-shot grids
+        sizes = [int(x) for x in os.environ["CHUNKS"].split(",")]
+        cases = [{"program": nm, "n": n, "variants": {
+            "policy": {}, "chunk2": {"chunk": 2}, "chunk4": {"chunk": 4},
+            "chunk8": {"chunk": 8}, "chunk4_t256": {"chunk": 4, "threads": 256}}}
+            for n in sizes for nm in ("p2", "c3_christoffel", "c1_dtg", "c2_maxwell", "p3",
+                                      "assign3", "outer3")]
     if os.environ.get("VNGROUPS"):  # output groups (Variant.vn) for the contractions
         sizes = [int(x) for x in os.environ["VNGROUPS"].split(",")]
         cases = [{"program": nm, "n": n, "variants": {
