@@ -322,6 +322,8 @@ int sp_mix1(const void* const* r, int nr, void* const* w, int nw, long long n, i
   if (nr == 40 && nw == 24) probe_mix1<40, 24><<<(unsigned)g, threads, 0, s>>>(P, n);
   else if (nr == 1 && nw == 1) probe_mix1<1, 1><<<(unsigned)g, threads, 0, s>>>(P, n);
   else if (nr == 5 && nw == 3) probe_mix1<5, 3><<<(unsigned)g, threads, 0, s>>>(P, n);
+  else if (nr == 16 && nw == 6) probe_mix1<16, 6><<<(unsigned)g, threads, 0, s>>>(P, n);
+  else if (nr == 24 && nw == 18) probe_mix1<24, 18><<<(unsigned)g, threads, 0, s>>>(P, n);
   else return -1;
   return (int)cudaGetLastError();
 }
@@ -335,6 +337,7 @@ int sp_mix(const void* const* r, int nr, void* const* w, int nw, long long n2, i
   if (nr == 40 && nw == 24) probe_mix<40, 24><<<g, 256, 0, s>>>(P, n2);
   else if (nr == 1 && nw == 1) probe_mix<1, 1><<<g, 256, 0, s>>>(P, n2);
   else if (nr == 5 && nw == 3) probe_mix<5, 3><<<g, 256, 0, s>>>(P, n2);
+  else if (nr == 16 && nw == 6) probe_mix<16, 6><<<g, 256, 0, s>>>(P, n2);
   else return -1;
   return (int)cudaGetLastError();
 }
