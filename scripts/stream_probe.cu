@@ -220,7 +220,13 @@ __global__ void __launch_bounds__(256) probe_mix1(const __grid_constant__ MixPtr
     }
 #pragma unroll
     for (int j = 0; j < W; ++j) __stcs(P.w[j] + i, s + j);
+    if (W == 0 && s < -1.0) P.w[0][i] = s;  // read-only mixes: keep the loads live
   }
+}
+
+// the dispatch floor of a one-shot grid: every thread exits at once
+__global__ void __launch_bounds__(256) probe_empty(long long n) {
+  if ((long long)blockIdx.x * blockDim.x + threadIdx.x == n) asm volatile("trap;");
 }
 
 static int sms() {
@@ -317,6 +323,11 @@ int sp_mix1(const void* const* r, int nr, void* const* w, int nw, long long n, i
   MixPtrs1 P;
   for (int j = 0; j < nr && j < 64; ++j) P.r[j] = (const double*)r[j];
   for (int j = 0; j < nw && j < 64; ++j) P.w[j] = (double*)w[j];
+  if (nw == 0) P.w[0] = (double*)w[0];  // never written (inputs are >= 0)
+  if (nr == 0) {  // no streams: the empty one-shot grid
+    probe_empty<<<(unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(n);
+    return (int)cudaGetLastError();
+  }
   long long g = blocks_per_sm > 0 ? (long long)sms() * blocks_per_sm : (n + threads - 1) / threads;
   cudaStream_t s = (cudaStream_t)stream;
   if (nr == 40 && nw == 24) probe_mix1<40, 24><<<(unsigned)g, threads, 0, s>>>(P, n);
@@ -324,6 +335,9 @@ int sp_mix1(const void* const* r, int nr, void* const* w, int nw, long long n, i
   else if (nr == 5 && nw == 3) probe_mix1<5, 3><<<(unsigned)g, threads, 0, s>>>(P, n);
   else if (nr == 16 && nw == 6) probe_mix1<16, 6><<<(unsigned)g, threads, 0, s>>>(P, n);
   else if (nr == 24 && nw == 18) probe_mix1<24, 18><<<(unsigned)g, threads, 0, s>>>(P, n);
+  else if (nr == 16 && nw == 0) probe_mix1<16, 0><<<(unsigned)g, threads, 0, s>>>(P, n);
+  else if (nr == 22 && nw == 0) probe_mix1<22, 0><<<(unsigned)g, threads, 0, s>>>(P, n);
+  else if (nr == 1 && nw == 0) probe_mix1<1, 0><<<(unsigned)g, threads, 0, s>>>(P, n);
   else return -1;
   return (int)cudaGetLastError();
 }
