@@ -85,7 +85,7 @@ struct Driver {
   CUresult (*MemcpyDtoHAsync)(void*, CUdeviceptr, size_t, CUstream) = nullptr;
   CUresult (*MemHostRegister)(void*, size_t, unsigned) = nullptr;
   CUresult (*MemHostUnregister)(void*) = nullptr;
-  CUresult (*PointerGetAttribute)(void*, CUpointer_attribute, CUdeviceptr) = nullptr;
+  CUresult (*PointerGetAttributes)(unsigned, CUpointer_attribute*, void**, CUdeviceptr) = nullptr;
   CUresult (*MemHostAlloc)(void**, size_t, unsigned) = nullptr;
   CUresult (*MemFreeHost)(void*) = nullptr;
   CUresult (*EventSynchronize)(CUevent) = nullptr;
@@ -177,7 +177,7 @@ int load_driver_locked() {
             bind(h, g_cu.MemcpyDtoHAsync, "cuMemcpyDtoHAsync_v2") &&
             bind(h, g_cu.MemHostRegister, "cuMemHostRegister_v2") &&
             bind(h, g_cu.MemHostUnregister, "cuMemHostUnregister") &&
-            bind(h, g_cu.PointerGetAttribute, "cuPointerGetAttribute") &&
+            bind(h, g_cu.PointerGetAttributes, "cuPointerGetAttributes") &&
             bind(h, g_cu.MemHostAlloc, "cuMemHostAlloc") &&
             bind(h, g_cu.MemFreeHost, "cuMemFreeHost") &&
             bind(h, g_cu.EventSynchronize, "cuEventSynchronize");
@@ -382,6 +382,18 @@ void release_stage_set(CtxState* st, StageSet* set) {
   st->stage_cv.notify_one();
 }
 
+// Whether `p` is memory the driver knows (device, cudaHostAlloc'd or
+// registered host memory).  cuPointerGetAttributes, unlike the singular
+// cuPointerGetAttribute, answers "unknown" (memory type 0) for plain
+// pageable memory without raising an API error — so sanitizer runs over
+// host-staged calls stay free of expected-error reports.
+bool driver_known(const void* p) {
+  unsigned int mt = 0;
+  CUpointer_attribute a = CU_POINTER_ATTRIBUTE_MEMORY_TYPE;
+  void* data[] = {&mt};
+  return g_cu.PointerGetAttributes(1, &a, data, (CUdeviceptr)p) == CUDA_SUCCESS && mt != 0;
+}
+
 // Page-lock pageable host ranges for the duration of one staged run
 // (TLB_HOST_REGISTER=1), so the copies are DMA'd directly instead of
 // through the driver's internal bounce buffers.  Ranges already pinned
@@ -414,10 +426,7 @@ void pin_host_ranges(std::vector<std::pair<uintptr_t, uintptr_t>> spans, HostPin
       merged.push_back(sp);
   }
   for (auto& m : merged) {
-    unsigned int mt = 0;
-    if (g_cu.PointerGetAttribute(&mt, CU_POINTER_ATTRIBUTE_MEMORY_TYPE, (CUdeviceptr)m.first) ==
-        CUDA_SUCCESS)
-      continue;  // already page-locked (or device memory)
+    if (driver_known((const void*)m.first)) continue;  // already page-locked (or device memory)
     void* p = (void*)m.first;
     if (g_cu.MemHostRegister(p, m.second - m.first, CU_MEMHOSTREGISTER_PORTABLE) == CUDA_SUCCESS)
       pins->regs.push_back(p);
@@ -965,12 +974,8 @@ int tlb_exec_host(tlb_kernel* k, long long n, const double* const* const* comp_p
   bool bounce = false;
   const bool do_register = host_register_enabled();
   if (!do_register) {
-    for (size_t j = 0; j < m && !bounce; ++j) {
-      unsigned int mt = 0;
-      const double* p = comp_ptrs[k->slot_field[j]][k->slot_comp[j]];
-      bounce = g_cu.PointerGetAttribute(&mt, CU_POINTER_ATTRIBUTE_MEMORY_TYPE,
-                                        (CUdeviceptr)p) != CUDA_SUCCESS;
-    }
+    for (size_t j = 0; j < m && !bounce; ++j)
+      bounce = !driver_known(comp_ptrs[k->slot_field[j]][k->slot_comp[j]]);
   }
   if (slab <= 0) {
     // nb buffers of m*slab doubles, at most ~4 GiB in total; bounced runs use
