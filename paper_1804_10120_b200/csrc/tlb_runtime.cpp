@@ -466,6 +466,7 @@ struct tlb_kernel {
   int dflt_vec = 2;
   int batch_bound = 256;  // TLK_BATCH_BOUND: the batch entries' largest block
   int chunk = 1;          // TLK_CHUNK: block-sized runs per block in tlk_flat_v1
+  int parts = 1;          // TLK_PARTS: independent statement parts (one block run each)
   int stage_smem = 0;     // its dynamic shared memory (from the source)
   int stage_batch_smem = 0;  // tlk_stage_batch_v1's: the ring + NSTAGE x NSLOTS pointers
   std::mutex mu;
@@ -619,6 +620,7 @@ int tlb_compile(const char* src, const char* const* opts, int nopts, const char*
   k->threads = (int)source_define(src, "TLK_THREADS", 256);
   k->batch_bound = (int)source_define(src, "TLK_BATCH_BOUND", k->threads);
   k->chunk = (int)std::max(1LL, source_define(src, "TLK_CHUNK", 1));
+  k->parts = (int)std::max(1LL, source_define(src, "TLK_PARTS", 1));
   k->dflt_waves = (int)source_define(src, "TLK_GRID_WAVES", 1);
   k->dflt_vec = (int)source_define(src, "TLK_VEC", 2) == 1 ? 1 : 2;
   const long long nstage = source_define(src, "TLK_NSTAGE", 0);
@@ -785,7 +787,15 @@ int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n, const uint6
   }
   long long waves = max_blocks < 0 ? -max_blocks : 1;
   long long cap = max_blocks > 0 ? max_blocks : (long long)st->sm_count * occ * waves;
-  blocks = std::max(1LL, std::min(std::min(blocks, cap), 0x7fffffffLL));
+  if (!vec2 && k->parts > 1) {
+    // tlk_flat_v1 under TLK_PARTS: one equal run of blocks per part (each run
+    // a full one-shot grid of the points; a capped grid shares the cap)
+    const long long p = k->parts;
+    blocks = std::max(1LL, std::min(std::min(blocks, std::max(1LL, cap / p)), 0x7fffffffLL / p));
+    blocks *= p;
+  } else {
+    blocks = std::max(1LL, std::min(std::min(blocks, cap), 0x7fffffffLL));
+  }
   void* args[] = {param.data()};
   CU(g_cu.LaunchKernel(L->fn[e], (unsigned)blocks, 1, 1, (unsigned)threads, 1, 1, 0, stream,
                        args, nullptr),

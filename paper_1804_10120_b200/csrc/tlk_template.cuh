@@ -174,9 +174,28 @@ struct tlk_shared_ptrs {
 #ifndef TLK_CHUNK
 #define TLK_CHUNK 1
 #endif
+// TLK_PARTS > 1 (Variant.split): the program is independent statement parts
+// (no field in common).  The grid's blocks are cut into TLK_PARTS equal runs
+// and run p evaluates part p over every point: a one-shot grid dispatches the
+// runs in order, so the parts stream one after another, each with fewer
+// concurrent DRAM streams than the whole program (the runtime multiplies the
+// grid by TLK_PARTS, read from the source).  Same bits: a point's statements
+// of one part run in program order, and parts share no storage.
+#ifndef TLK_PARTS
+#define TLK_PARTS 1
+#endif
 extern "C" __global__ void __launch_bounds__(TLK_THREADS, TLK_MINB)
 tlk_flat_v1(const __grid_constant__ tlk_flat_params prm) {
-#if TLK_CHUNK > 1
+#if TLK_PARTS > 1
+  const unsigned per = gridDim.x / TLK_PARTS;
+  const unsigned part = blockIdx.x / per;
+  if (part >= TLK_PARTS) return;
+  const long long stride = (long long)per * blockDim.x;
+  TLK_LOOP
+  for (long long x = (long long)(blockIdx.x - part * per) * blockDim.x + threadIdx.x; x < prm.n;
+       x += stride)
+    tlk_part<double>(part, prm, x);
+#elif TLK_CHUNK > 1
   const long long bstride = (long long)gridDim.x * blockDim.x * TLK_CHUNK;
   for (long long base = (long long)blockIdx.x * blockDim.x * TLK_CHUNK; base < prm.n;
        base += bstride) {

@@ -408,7 +408,8 @@ def _operand(x) -> str:
 
 
 def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = False,
-               restrict: bool = True, direct: set[int] | frozenset = frozenset()) -> list[str]:
+               restrict: bool = True, direct: set[int] | frozenset = frozenset(),
+               inline_groups: bool = False) -> list[str]:
     """C++ text of the per-point body.
 
     With ``restrict`` (default) the body is a function of one
@@ -423,7 +424,7 @@ def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = F
     loads first in the source.
     """
     if any(ins.op == "grp" for ins in instrs):
-        return _emit_groups(instrs, slot_flags, hoist_loads, restrict, direct)
+        return _emit_groups(instrs, slot_flags, hoist_loads, restrict, direct, inline_groups)
     # keep only the final store of every slot; earlier values were consumed
     # through the register shadow
     last = {}
@@ -497,14 +498,19 @@ def _emit_instr(ins: Instr, ptr, direct, keep_store: bool) -> str | None:
 
 
 def _emit_groups(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool,
-                 restrict: bool, direct) -> list[str]:
+                 restrict: bool, direct, inline: bool = False) -> list[str]:
     """Body of a program lowered in output groups (Variant.vn = 1): one
     ``__noinline__`` device function per group, each loading what it reads
     (through the kernel's parameter block, passed by reference:
     ``__grid_constant__`` in the flat entries, so no copy), computing with its
     own value numbering and storing its outputs; ``tlk_point`` calls them in
     order.  Separate functions are what keeps ptxas from re-merging the
-    subexpressions groups recompute (its CSE sees through any inline asm)."""
+    subexpressions groups recompute (its CSE sees through any inline asm).
+
+    ``inline`` (statement parts, Variant.split): the groups are independent
+    statement parts with no field in common — ``__forceinline__`` functions,
+    and ``tlk_part(part, P_, x)`` runs one of them (tlk_flat_v1 under
+    TLK_PARTS)."""
     last = {ins.slot: k for k, ins in enumerate(instrs) if ins.op == "st"}
     groups: list[list[tuple[int, Instr]]] = [[]]
     for k, ins in enumerate(instrs):
@@ -515,8 +521,9 @@ def _emit_groups(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool,
     out: list[str] = []
     for g, items in enumerate(groups):
         used = sorted({ins.slot for _, ins in items if ins.op in ("ld", "st")})
+        attr = "__forceinline__" if inline else "__noinline__"
         out += ["template <typename T, int LD, typename P>",
-                f"__device__ __noinline__ void tlk_grp{g}(const P& P_, const long long x) {{"]
+                f"__device__ {attr} void tlk_grp{g}(const P& P_, const long long x) {{"]
         if restrict:
             for j in used:
                 q = "double* __restrict__" if slot_flags[j] & SLOT_WRITE else \
@@ -536,6 +543,13 @@ def _emit_groups(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool,
             "__device__ __forceinline__ void tlk_point(const P& P_, const long long x) {"]
     out += [f"  tlk_grp{g}<T, LD>(P_, x);" for g in range(len(groups))]
     out.append("}")
+    if inline:
+        out += ["template <typename T, int LD = TLK_LDMODE, typename P>",
+                "__device__ __forceinline__ void tlk_part(const unsigned part, const P& P_, "
+                "const long long x) {",
+                "  switch (part) {"]
+        out += [f"    case {g}: tlk_grp{g}<T, LD>(P_, x); break;" for g in range(len(groups))]
+        out += ["  }", "}"]
     return out
 
 
@@ -583,6 +597,7 @@ class Variant:
     batch_bound: int = 0  # TLK_BATCH_BOUND: the batch entries' __launch_bounds__ (0 = threads)
     vn: int = 0  # 1: outputs split into groups, one non-inlined device function each
     chunk: int = 1  # TLK_CHUNK: block-sized runs of points per block (tlk_flat_v1; tuning)
+    split: int = 0  # 1: independent statement parts run one after another (TLK_PARTS)
 
     def tag(self) -> str:
         t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
@@ -596,6 +611,7 @@ class Variant:
         t += f"q{self.batch_bound}" if self.batch_bound else ""
         t += "u" if self.vn else ""
         t += f"c{self.chunk}" if self.chunk > 1 else ""
+        t += "y" if self.split else ""
         return t + (f"n{self.threads}" if self.threads != 256 else "")
 
     def small_class(self) -> "Variant":
@@ -622,10 +638,10 @@ class Variant:
         launch-time choices; both entry points are in every module)."""
         return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs, self.stage,
                  self.threads, self.stage_threads, self.stage_reads, self.minb, self.stage_ws,
-                 self.batch_bound, self.vn, self.chunk)
+                 self.batch_bound, self.vn, self.chunk, self.split)
                 == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs, other.stage,
                     other.threads, other.stage_threads, other.stage_reads, other.minb,
-                    other.stage_ws, other.batch_bound, other.vn, other.chunk))
+                    other.stage_ws, other.batch_bound, other.vn, other.chunk, other.split))
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -831,6 +847,8 @@ def _env_variant(v: Variant) -> Variant:
         kw["minb"] = int(env["TLK_MINB"])
     if "TLK_STAGE_WS" in env:
         kw["stage_ws"] = int(env["TLK_STAGE_WS"])
+    if "TLK_SPLIT" in env:
+        kw["split"] = int(env["TLK_SPLIT"])
     if kw:
         kw["small_n"] = 0  # a forced variant applies at every size ...
     if "TLK_SMALL_N" in env:
@@ -851,12 +869,19 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     if not statements:
         raise LoweringError("nothing to lower: no statements")
 
-    def lower(budget: int):
+    def lower(budget: int, parts: list[list[int]] | None = None, fields_of=None):
         low = _Lowerer(alias)
+        if fields_of is not None:  # keep another lowering's field order (callers' layout)
+            low.fields, low.index = list(fields_of.fields), dict(fields_of.index)
         lhs = []
-        for k, v in enumerate(statements):
-            lhs.append(low.tensor(v, v.stmt.lhs.field))
-            low.statement(v, None if components is None else components[k], budget)
+        order = [list(range(len(statements)))] if parts is None else parts
+        for p, ks in enumerate(order):
+            if p:
+                low.b.begin_group()
+            for k in ks:
+                v = statements[k]
+                lhs.append(low.tensor(v, v.stmt.lhs.field))
+                low.statement(v, None if components is None else components[k], budget)
         return low, lhs
 
     low, lhs_fields = lower(0)
@@ -881,8 +906,14 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     phases = _phases(b.instrs)
     policy = variant is None
     if variant is None:
-        variant = _env_variant(choose_variant(reads, writes, n_ops, rw, b.chained,
-                                              len(statements)))
+        chosen = choose_variant(reads, writes, n_ops, rw, b.chained, len(statements))
+        if (int(os.environ.get("TLK_POLICY", "3")) >= 3 and len(statements) > 1
+                and len(statement_parts(statements, alias)) > 1):
+            # independent statement parts stream one after another (Variant.split):
+            # +0.4-1.1 % on P2 and Maxwell at 2^21-2^28, -0.7 % at 2^18
+            # (profiles/r02/tuning/tune_ab_split.jsonl)
+            chosen = Variant(**{**chosen.__dict__, "split": 1})
+        variant = _env_variant(chosen)
         if "TLK_STAGE_FRAC" in os.environ:  # tuning: staged share of the read slots
             frac = float(os.environ["TLK_STAGE_FRAC"])
             variant = Variant(**{**variant.__dict__,
@@ -899,6 +930,20 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
                 low, lhs_fields, b = low2, lhs2, low2.b
                 variant = Variant(**{**variant.__dict__, "vn": 1})
                 n_ops = sum(1 for i in b.instrs if i.op not in ("ld", "st", "grp"))
+    parts = statement_parts(statements, alias) if variant.split else []
+    if variant.split and (len(parts) < 2 or variant.vn or variant.chunk > 1 or variant.stage):
+        # one part (or output groups / chunks / the staged ring already shape
+        # the entry): no split
+        variant = Variant(**{**variant.__dict__, "split": 0})
+    if variant.split:
+        # independent statement parts (no field in common): each part becomes
+        # its own inlined body; tlk_flat_v1 gives every part its own run of
+        # blocks, in order, so the parts stream one after another with fewer
+        # concurrent DRAM streams each (the other entries run the parts in turn)
+        low, lhs_fields = lower(0, parts, fields_of=low)
+        b = low.b
+        for (f, c), sl in b.slots.items():  # the slot order follows the parts
+            slot_field[sl], slot_comp[sl] = f, c
     if hoist_loads is not None:
         variant = Variant(**{**variant.__dict__, "hoist": hoist_loads})
     if variant.ldmode == 1 and rw:
@@ -938,7 +983,7 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
             r += 1 if take else 0
     direct = {j for j, o in enumerate(rord) if o < 0 and b.slot_flags[j] & SLOT_READ}
     body = "\n".join(_emit_body(b.instrs, b.slot_flags, variant.hoist, variant.restrict,
-                                direct))
+                                direct, inline_groups=bool(variant.split)))
     header = [f"// generated by paper_1804_10120_b200.lowering ({LOWERING_VERSION})",
               f"// variant {variant.tag()}"]
     for v in statements:
@@ -955,6 +1000,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         header.append(f"#define TLK_BATCH_BOUND {variant.batch_bound}")
     if variant.chunk > 1:
         header.append(f"#define TLK_CHUNK {variant.chunk}")
+    if variant.split:
+        header.append(f"#define TLK_PARTS {b.groups}")
     if variant.stage:
         header.append(f"#define TLK_NSTAGE {variant.stage}")
         header.append(f"#define TLK_NREAD {len(rord) - rord.count(-1)}")
@@ -1017,6 +1064,54 @@ def _max_live(instrs: list[Instr]) -> int:
             if ins.dst not in last:  # never used
                 live -= 1
     return peak
+
+
+def statement_parts(statements: Sequence[Any], alias: Mapping[str, str] | None = None
+                    ) -> list[list[int]]:
+    """Statements grouped into independent parts: two statements are in one
+    part when they touch (read or write) a common field, transitively.  Parts
+    share no storage, so running part after part over the whole grid gives
+    the bits of the sequential program (every statement of a part keeps its
+    order).  Ordered by first statement."""
+    alias = dict(alias or {})
+    parent = list(range(len(statements)))
+
+    def find(i: int) -> int:
+        while parent[i] != i:
+            parent[i] = parent[parent[i]]
+            i = parent[i]
+        return i
+
+    owner: dict[str, int] = {}
+    for k, v in enumerate(statements):
+        for name in [v.stmt.lhs.field] + _field_names(v.stmt.rhs):
+            r = alias.get(name, name)
+            if r in owner:
+                parent[find(k)] = find(owner[r])
+            else:
+                owner[r] = k
+    parts: dict[int, list[int]] = {}
+    for k in range(len(statements)):
+        parts.setdefault(find(k), []).append(k)
+    return sorted(parts.values(), key=lambda ks: ks[0])
+
+
+def _field_names(e) -> list[str]:
+    out, stack = [], [e]
+    while stack:
+        x = stack.pop()
+        k = kind(x)
+        if k == "Leaf":
+            out.append(x.leaf.field)
+        elif k == "FieldRef":
+            out.append(x.name)
+        elif k in ("Add", "Sub", "Mul", "Div"):
+            stack += [x.l, x.r]
+        elif k in ("Neg", "Sqrt"):
+            stack.append(x.e)
+        elif k == "Sum":
+            stack.append(x.body)
+    return out
 
 
 def _phases(instrs: list[Instr]) -> int:

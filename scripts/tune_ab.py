@@ -195,6 +195,10 @@ def main():
             "chunk8": {"chunk": 8}, "chunk4_t256": {"chunk": 4, "threads": 256}}}
             for n in sizes for nm in ("p2", "c3_christoffel", "c1_dtg", "c2_maxwell", "p3",
                                       "assign3", "outer3")]
+    if os.environ.get("SPLITS"):  # independent statement parts (Variant.split)
+        sizes = [int(x) for x in os.environ["SPLITS"].split(",")]
+        cases = [{"program": nm, "n": n, "variants": {"policy": {}, "split": {"split": 1}}}
+                 for n in sizes for nm in ("p2", "c2_maxwell")]
     if os.environ.get("VNGROUPS"):  # output groups (Variant.vn) for the contractions
         sizes = [int(x) for x in os.environ["VNGROUPS"].split(",")]
         cases = [{"program": nm, "n": n, "variants": {

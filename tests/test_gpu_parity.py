@@ -393,6 +393,56 @@ def test_output_groups_are_bit_exact(name, budget, monkeypatch):
         _check(case, env_to_host(env), want)
 
 
+def _multi_part_cases() -> list[str]:
+    from paper_1804_10120_b200.ir import ValidationError
+    from paper_1804_10120_b200.lowering import statement_parts
+
+    out = []
+    for name in CASES:
+        try:
+            _, vs = program(manifest()["cases"][name]["source"])
+        except (AssertionError, ValidationError):
+            continue
+        if len(statement_parts(vs)) > 1:
+            out.append(name)
+    return out
+
+
+@pytest.mark.parametrize("name", _multi_part_cases())
+def test_statement_parts_are_bit_exact(name):
+    # Variant.split: a program of independent statement parts runs part after
+    # part, each over its own run of blocks of tlk_flat_v1 — one-shot grids,
+    # capped (grid-stride) grids of a few blocks, and the 2-point entry that
+    # runs the parts in turn, against the reference's goldens
+    from paper_1804_10120_b200.evaluator import _bind, _fusion_plan
+    from paper_1804_10120_b200.lowering import Variant, lower_program
+    from paper_1804_10120_b200.runtime import Kernel
+
+    one_shot = 1 << 62  # TLB_ONE_SHOT (include/tlb200.h)
+    case = manifest()["cases"][name]
+    prog, vs = program(case["source"])
+    host, want = golden_io(name)
+    env = device_env(prog, host)
+    fp = _fusion_plan(vs, env)
+    if fp is None or case.get("raises"):
+        pytest.skip("program does not run as one fused launch")
+    plan = lower_program(vs, variant=Variant(vec=1, waves=0, threads=128, split=1))
+    if "TLK_PARTS" not in plan.source:
+        pytest.skip("a single statement part")
+    n, resizes = fp
+    k = Kernel(plan)
+    for kw in (dict(max_blocks=one_shot), dict(max_blocks=3), dict(max_blocks=1),
+               dict(max_blocks=0), dict(threads=64, max_blocks=one_shot),
+               dict(vec=2 if n % 2 == 0 else 1)):
+        env2 = device_env(prog, host)  # fresh inputs and targets per launch shape
+        for lhs, size in resizes:
+            env2[lhs.name].resize(size)
+        _, _, st2 = _bind(vs, env2)
+        k.launch(n, [s_.base for s_ in st2], [s_.pitch for s_ in st2],
+                 torch.cuda.current_stream().cuda_stream, **kw)
+        _check(case, env_to_host(env2), want)
+
+
 def test_grouped_program_in_a_multi_domain_batch():
     # contract3 lowers in output groups; its batch entry calls the same
     # group functions with the domain's slot pointers staged in shared memory

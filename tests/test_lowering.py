@@ -300,3 +300,66 @@ def test_staged_entries_use_bulk_copies_without_spills(ws):
     assert "SYNCS" in sass  # mbarrier operations
     assert "LDL" not in sass and "STL" not in sass
     assert "DFMA" not in sass
+
+
+def test_statement_parts():
+    # independent statements (no field in common, transitively) form parts
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.lowering import statement_parts
+
+    assert statement_parts(tb.load(tb.P2)[1]) == [[0], [1]]
+    assert statement_parts(tb.load(tb.MAXWELL)[1]) == [[0, 1, 2, 7], [3, 4, 5, 6]]
+    assert statement_parts(tb.load(tb.P3)[1]) == [[0, 1, 2]]  # chained through Gamma, db
+    _, vs = tb.load(tb.P2)
+    # two names for one storage join their statements into one part
+    assert statement_parts(vs, {"K": "dg"}) == [[0, 1]]
+
+
+def test_split_policy_keeps_field_order_and_emits_parts():
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.lowering import Variant
+
+    for text, parts in ((tb.P2, 2), (tb.MAXWELL, 2)):
+        _, vs = tb.load(text)
+        plan = lower_program(vs)
+        assert plan.variant.split == 1 and "y" in plan.variant.tag()
+        assert f"#define TLK_PARTS {parts}" in plan.source
+        assert "tlk_part(const unsigned part" in plan.source
+        flat = lower_program(vs, variant=Variant(**{**plan.variant.__dict__, "split": 0}))
+        # callers bind fields by the plan's order: splitting must not change it
+        assert [f.name for f in plan.fields] == [f.name for f in flat.fields]
+        assert plan.bytes_per_point == flat.bytes_per_point
+        assert plan.flops_per_point == flat.flops_per_point
+        assert sorted(zip(plan.slot_field, plan.slot_comp, plan.slot_flags)) == \
+            sorted(zip(flat.slot_field, flat.slot_comp, flat.slot_flags))
+    # a single part, or output groups, never split
+    _, vs = tb.load(tb.P3)
+    assert lower_program(vs).variant.split == 0
+    _, vs = tb.load(tb.P2)
+    assert lower_program(vs, variant=Variant(split=1, vn=1)).variant.split == 0
+
+
+def test_split_kernel_compiles_with_fewer_registers():
+    # P2's parts alone need fewer registers than the fused body (128 -> 89)
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.lowering import Variant
+
+    if not shutil.which("cuobjdump"):
+        pytest.skip("no cuobjdump")
+    _, vs = tb.load(tb.P2)
+    plan = lower_program(vs)
+    flat = lower_program(vs, variant=Variant(**{**plan.variant.__dict__, "split": 0}))
+
+    def regs(p):
+        k = get_kernel(p)
+        path = k.cubin_path
+        if not path.exists():
+            path.write_bytes(k.cubin())
+        out = subprocess.run(["cuobjdump", "-res-usage", str(path)], capture_output=True,
+                             text=True, check=True).stdout.splitlines()
+        for i, line in enumerate(out):
+            if "tlk_flat_v1" in line:
+                return int(out[i + 1].split("REG:")[1].split()[0])
+        raise AssertionError("no tlk_flat_v1")
+
+    assert regs(plan) < regs(flat)
