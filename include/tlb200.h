@@ -109,6 +109,10 @@ int tlb_kernel_attrs(tlb_kernel* k, const char* entry, int* regs, int* local_byt
  * threads: block size (0 = the kernel's compiled TLK_THREADS; must not
  * exceed it).  max_blocks: grid cap (0 = one full wave at occupancy, -w = w
  * waves, > 0 that many blocks at most, >= TLB_ONE_SHOT a one-shot grid).
+ * Modules lowered in independent statement parts (TLK_PARTS = p > 1 in the
+ * source) run the 1-point entry as p equal runs of blocks, one per part: the
+ * grid above is computed per part (a cap is shared, at least one block per
+ * part) and multiplied by p.
  * Asynchronous on `stream`. */
 int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
                const long long* pitches, int vec, int threads, long long max_blocks,

@@ -408,8 +408,7 @@ def _operand(x) -> str:
 
 
 def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = False,
-               restrict: bool = True, direct: set[int] | frozenset = frozenset(),
-               inline_groups: bool = False) -> list[str]:
+               restrict: bool = True, direct: set[int] | frozenset = frozenset()) -> list[str]:
     """C++ text of the per-point body.
 
     With ``restrict`` (default) the body is a function of one
@@ -424,7 +423,7 @@ def _emit_body(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool = F
     loads first in the source.
     """
     if any(ins.op == "grp" for ins in instrs):
-        return _emit_groups(instrs, slot_flags, hoist_loads, restrict, direct, inline_groups)
+        return _emit_groups(instrs, slot_flags, hoist_loads, restrict, direct)
     # keep only the final store of every slot; earlier values were consumed
     # through the register shadow
     last = {}
@@ -498,7 +497,7 @@ def _emit_instr(ins: Instr, ptr, direct, keep_store: bool) -> str | None:
 
 
 def _emit_groups(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool,
-                 restrict: bool, direct, inline: bool = False) -> list[str]:
+                 restrict: bool, direct, inline: bool = False, point: bool = True) -> list[str]:
     """Body of a program lowered in output groups (Variant.vn = 1): one
     ``__noinline__`` device function per group, each loading what it reads
     (through the kernel's parameter block, passed by reference:
@@ -510,7 +509,7 @@ def _emit_groups(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool,
     ``inline`` (statement parts, Variant.split): the groups are independent
     statement parts with no field in common — ``__forceinline__`` functions,
     and ``tlk_part(part, P_, x)`` runs one of them (tlk_flat_v1 under
-    TLK_PARTS)."""
+    TLK_PARTS); ``point=False`` leaves ``tlk_point`` to the fused body."""
     last = {ins.slot: k for k, ins in enumerate(instrs) if ins.op == "st"}
     groups: list[list[tuple[int, Instr]]] = [[]]
     for k, ins in enumerate(instrs):
@@ -539,10 +538,11 @@ def _emit_groups(instrs: list[Instr], slot_flags: list[int], hoist_loads: bool,
             if line is not None:
                 out.append(line)
         out.append("}")
-    out += ["template <typename T, int LD = TLK_LDMODE, typename P>",
-            "__device__ __forceinline__ void tlk_point(const P& P_, const long long x) {"]
-    out += [f"  tlk_grp{g}<T, LD>(P_, x);" for g in range(len(groups))]
-    out.append("}")
+    if point:
+        out += ["template <typename T, int LD = TLK_LDMODE, typename P>",
+                "__device__ __forceinline__ void tlk_point(const P& P_, const long long x) {"]
+        out += [f"  tlk_grp{g}<T, LD>(P_, x);" for g in range(len(groups))]
+        out.append("}")
     if inline:
         out += ["template <typename T, int LD = TLK_LDMODE, typename P>",
                 "__device__ __forceinline__ void tlk_part(const unsigned part, const P& P_, "
@@ -869,10 +869,14 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
     if not statements:
         raise LoweringError("nothing to lower: no statements")
 
-    def lower(budget: int, parts: list[list[int]] | None = None, fields_of=None):
+    def lower(budget: int, parts: list[list[int]] | None = None, layout_of=None):
         low = _Lowerer(alias)
-        if fields_of is not None:  # keep another lowering's field order (callers' layout)
-            low.fields, low.index = list(fields_of.fields), dict(fields_of.index)
+        if layout_of is not None:
+            # keep another lowering's field order (the callers' layout) and slot
+            # numbering (one parameter block serves both lowerings' bodies)
+            low.fields, low.index = list(layout_of.fields), dict(layout_of.index)
+            low.b.slots = dict(layout_of.b.slots)
+            low.b.slot_flags = [0] * len(layout_of.b.slots)
         lhs = []
         order = [list(range(len(statements)))] if parts is None else parts
         for p, ks in enumerate(order):
@@ -940,10 +944,10 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         # its own inlined body; tlk_flat_v1 gives every part its own run of
         # blocks, in order, so the parts stream one after another with fewer
         # concurrent DRAM streams each (the other entries run the parts in turn)
-        low, lhs_fields = lower(0, parts, fields_of=low)
+        fused = b  # the whole program's body: tlk_point, for every other entry
+        low, lhs_fields = lower(0, parts, layout_of=low)
         b = low.b
-        for (f, c), sl in b.slots.items():  # the slot order follows the parts
-            slot_field[sl], slot_comp[sl] = f, c
+        assert b.slots == fused.slots and b.slot_flags == fused.slot_flags
     if hoist_loads is not None:
         variant = Variant(**{**variant.__dict__, "hoist": hoist_loads})
     if variant.ldmode == 1 and rw:
@@ -982,8 +986,17 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
             rord.append(r if take else -1)
             r += 1 if take else 0
     direct = {j for j, o in enumerate(rord) if o < 0 and b.slot_flags[j] & SLOT_READ}
-    body = "\n".join(_emit_body(b.instrs, b.slot_flags, variant.hoist, variant.restrict,
-                                direct, inline_groups=bool(variant.split)))
+    if variant.split:
+        # tlk_part (the parts, tlk_flat_v1's split runs) beside the fused
+        # tlk_point that the 2-point, batch and staged entries keep: run per
+        # point in turn, the parts cost C4's batch entry 23 % (160 -> 199 us)
+        body = "\n".join(_emit_groups(b.instrs, b.slot_flags, variant.hoist, variant.restrict,
+                                      direct, inline=True, point=False)
+                         + _emit_body(fused.instrs, fused.slot_flags, variant.hoist,
+                                      variant.restrict, direct))
+    else:
+        body = "\n".join(_emit_body(b.instrs, b.slot_flags, variant.hoist, variant.restrict,
+                                    direct))
     header = [f"// generated by paper_1804_10120_b200.lowering ({LOWERING_VERSION})",
               f"// variant {variant.tag()}"]
     for v in statements:

@@ -199,6 +199,12 @@ def main():
         sizes = [int(x) for x in os.environ["SPLITS"].split(",")]
         cases = [{"program": nm, "n": n, "variants": {"policy": {}, "split": {"split": 1}}}
                  for n in sizes for nm in ("p2", "c2_maxwell")]
+    if os.environ.get("SPLIT_THREADS"):  # block size of split programs (policy: split)
+        sizes = [int(x) for x in os.environ["SPLIT_THREADS"].split(",")]
+        cases = [{"program": nm, "n": n, "variants": {
+            "policy": {}, "nosplit": {"split": 0}, "split_t128": {"threads": 128},
+            "split_t256": {"threads": 256}, "split_t512": {"threads": 512}}}
+            for n in sizes for nm in ("p2", "c2_maxwell")]
     if os.environ.get("VNGROUPS"):  # output groups (Variant.vn) for the contractions
         sizes = [int(x) for x in os.environ["VNGROUPS"].split(",")]
         cases = [{"program": nm, "n": n, "variants": {
