@@ -72,6 +72,12 @@ while time.time() < t_end:
         torch.cuda.synchronize()
         got = env_to_host(env)
         stats["cases"] += 1
+        try:  # programs the policy runs as independent statement parts
+            from paper_1804_10120_b200.evaluator import plan_for
+
+            stats["split"] = stats.get("split", 0) + plan_for(stmts, env).variant.split
+        except Exception:
+            pass
         if n <= 1 << 19:
             want = {key: a.copy() for key, a in host.items()}
             numpy_eval.eval_program(stmts, want)
