@@ -467,6 +467,7 @@ struct tlb_kernel {
   int batch_bound = 256;  // TLK_BATCH_BOUND: the batch entries' largest block
   int chunk = 1;          // TLK_CHUNK: block-sized runs per block in tlk_flat_v1
   int parts = 1;          // TLK_PARTS: independent statement parts (one block run each)
+  int batch_parts = 1;    // ... run as (part, domain) row runs by tlk_batch_v1 (TLK_BATCH_SPLIT)
   int stage_smem = 0;     // its dynamic shared memory (from the source)
   int stage_batch_smem = 0;  // tlk_stage_batch_v1's: the ring + NSTAGE x NSLOTS pointers
   std::mutex mu;
@@ -621,6 +622,7 @@ int tlb_compile(const char* src, const char* const* opts, int nopts, const char*
   k->batch_bound = (int)source_define(src, "TLK_BATCH_BOUND", k->threads);
   k->chunk = (int)std::max(1LL, source_define(src, "TLK_CHUNK", 1));
   k->parts = (int)std::max(1LL, source_define(src, "TLK_PARTS", 1));
+  k->batch_parts = source_define(src, "TLK_BATCH_SPLIT", 0) ? k->parts : 1;
   k->dflt_waves = (int)source_define(src, "TLK_GRID_WAVES", 1);
   k->dflt_vec = (int)source_define(src, "TLK_VEC", 2) == 1 ? 1 : 2;
   const long long nstage = source_define(src, "TLK_NSTAGE", 0);
@@ -921,7 +923,7 @@ int tlb_batch_launch(tlb_batch* b, int vec, int threads, void* stream) {
                 b->k->batch_bound);
   long long units = v2 ? (b->max_n + 1) / 2 : b->max_n;
   long long gx = std::max(1LL, (units + threads - 1) / threads);
-  long long gy = std::min<long long>(b->ndom, 65535);
+  long long gy = std::min<long long>((long long)b->ndom * (v2 ? 1 : b->k->batch_parts), 65535);
   // optional cap of the grid at a few waves (TLB_BATCH_WAVES; default 0 =
   // one block per (domain, chunk): measured 190 us vs 195 us at 4 waves for
   // C4); capped blocks loop over x chunks and domains

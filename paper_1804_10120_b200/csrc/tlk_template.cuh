@@ -258,9 +258,47 @@ __device__ __forceinline__ void tlk_domain(const P& ptrs, const long long n, con
   }
 }
 
+#if defined(TLK_BATCH_SPLIT) && TLK_PARTS > 1
+// the 1-point batch entry over statement parts: block rows y walk (part,
+// domain) pairs part-major, so every domain's part 0 streams before any
+// part 1 (the runtime launches ndom x TLK_PARTS rows, capped at 65535)
+template <typename P>
+__device__ __forceinline__ void tlk_domain_part(const unsigned part, const P& ptrs,
+                                                const long long n, const long long stride) {
+  TLK_LOOP
+  for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += stride)
+    tlk_part<double>(part, ptrs, x);
+}
+#endif
+
 template <typename T>
 __device__ __forceinline__ void tlk_batch_body(const long long* __restrict__ table, int ndom) {
   const long long stride = (long long)gridDim.x * blockDim.x;
+#if defined(TLK_BATCH_SPLIT) && TLK_PARTS > 1
+  if constexpr (sizeof(T) == 8) {
+    const int rows = ndom * TLK_PARTS;
+#if TLK_BATCH_PTRS == 0
+    __shared__ double* spp[TLK_NSLOTS];
+#endif
+    for (int y = blockIdx.y; y < rows; y += gridDim.y) {
+      const unsigned part = (unsigned)(y / ndom);
+      const int d = y - (int)part * ndom;
+      const long long* rec = table + (long long)d * (TLK_NSLOTS + 1);
+#if TLK_BATCH_PTRS == 0
+      __syncthreads();
+      for (int j = threadIdx.x; j < TLK_NSLOTS; j += blockDim.x)
+        spp[j] = reinterpret_cast<double*>(rec[1 + j]);
+      const long long n = rec[0];
+      __syncthreads();
+      tlk_domain_part(part, tlk_shared_ptrs{spp}, n, stride);
+#else
+      const tlk_table_ptrs P{rec, {rec}};
+      tlk_domain_part(part, P, __ldg(rec), stride);
+#endif
+    }
+    return;
+  }
+#endif
 #if TLK_BATCH_PTRS == 0
   __shared__ double* sp[TLK_NSLOTS];
   for (int d = blockIdx.y; d < ndom; d += gridDim.y) {

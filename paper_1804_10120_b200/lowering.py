@@ -598,6 +598,7 @@ class Variant:
     vn: int = 0  # 1: outputs split into groups, one non-inlined device function each
     chunk: int = 1  # TLK_CHUNK: block-sized runs of points per block (tlk_flat_v1; tuning)
     split: int = 0  # 1: independent statement parts run one after another (TLK_PARTS)
+    batch_split: int = 0  # 1: the 1-point batch entry runs the parts as row runs too
 
     def tag(self) -> str:
         t = (f"r{int(self.restrict)}h{int(self.hoist)}l{self.ldmode}"
@@ -612,6 +613,7 @@ class Variant:
         t += "u" if self.vn else ""
         t += f"c{self.chunk}" if self.chunk > 1 else ""
         t += "y" if self.split else ""
+        t += "z" if self.split and self.batch_split else ""
         return t + (f"n{self.threads}" if self.threads != 256 else "")
 
     def small_class(self) -> "Variant":
@@ -638,10 +640,11 @@ class Variant:
         launch-time choices; both entry points are in every module)."""
         return ((self.restrict, self.hoist, self.ldmode, self.batch_ptrs, self.stage,
                  self.threads, self.stage_threads, self.stage_reads, self.minb, self.stage_ws,
-                 self.batch_bound, self.vn, self.chunk, self.split)
+                 self.batch_bound, self.vn, self.chunk, self.split, self.batch_split)
                 == (other.restrict, other.hoist, other.ldmode, other.batch_ptrs, other.stage,
                     other.threads, other.stage_threads, other.stage_reads, other.minb,
-                    other.stage_ws, other.batch_bound, other.vn, other.chunk, other.split))
+                    other.stage_ws, other.batch_bound, other.vn, other.chunk, other.split,
+                    other.batch_split))
 
 
 def choose_variant(reads: int, writes: int, n_ops: int, rw_slots: int,
@@ -849,6 +852,8 @@ def _env_variant(v: Variant) -> Variant:
         kw["stage_ws"] = int(env["TLK_STAGE_WS"])
     if "TLK_SPLIT" in env:
         kw["split"] = int(env["TLK_SPLIT"])
+    if "TLK_BATCH_SPLIT" in env:
+        kw["batch_split"] = int(env["TLK_BATCH_SPLIT"])
     if kw:
         kw["small_n"] = 0  # a forced variant applies at every size ...
     if "TLK_SMALL_N" in env:
@@ -1015,6 +1020,8 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         header.append(f"#define TLK_CHUNK {variant.chunk}")
     if variant.split:
         header.append(f"#define TLK_PARTS {b.groups}")
+        if variant.batch_split:
+            header.append("#define TLK_BATCH_SPLIT 1")
     if variant.stage:
         header.append(f"#define TLK_NSTAGE {variant.stage}")
         header.append(f"#define TLK_NREAD {len(rord) - rord.count(-1)}")
