@@ -950,9 +950,11 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         # blocks, in order, so the parts stream one after another with fewer
         # concurrent DRAM streams each (the other entries run the parts in turn)
         fused = b  # the whole program's body: tlk_point, for every other entry
-        low, lhs_fields = lower(0, parts, layout_of=low)
-        b = low.b
-        assert b.slots == fused.slots and b.slot_flags == fused.slot_flags
+        low2, lhs2 = lower(0, parts, layout_of=low)
+        if low2.b.slots == fused.slots and low2.b.slot_flags == fused.slot_flags:
+            low, lhs_fields, b = low2, lhs2, low2.b
+        else:  # one parameter block must serve both bodies; never expected
+            variant = Variant(**{**variant.__dict__, "split": 0})
     if hoist_loads is not None:
         variant = Variant(**{**variant.__dict__, "hoist": hoist_loads})
     if variant.ldmode == 1 and rw:
@@ -992,7 +994,7 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
             r += 1 if take else 0
     direct = {j for j, o in enumerate(rord) if o < 0 and b.slot_flags[j] & SLOT_READ}
     if variant.split:
-        # tlk_part (the parts, tlk_flat_v1's split runs) beside the fused
+        # tlk_part (the parts: tlk_flat_v1's split runs) beside the fused
         # tlk_point that the 2-point, batch and staged entries keep: run per
         # point in turn, the parts cost C4's batch entry 23 % (160 -> 199 us)
         body = "\n".join(_emit_groups(b.instrs, b.slot_flags, variant.hoist, variant.restrict,
