@@ -505,11 +505,46 @@ def run_e2e(args, dist: Dist, vs, n_local: int) -> dict:
     dt = dist.allreduce(time.perf_counter() - t0, "max") / args.e2e_steps
     h2d = 8 * plan.reads * n_local
     d2h = 8 * plan.writes * n_local
-    return {"value": args.points / dt, "unit": "gridpoints/s",
-            "h2d_bytes_per_step": h2d * dist.world, "d2h_bytes_per_step": d2h * dist.world,
-            "s_per_step": round(dt, 4), "steps": args.e2e_steps,
-            "path": "eval_program(pinned host fields) -> tlb_exec_host: H2D -> fused kernel "
-                    f"-> D2H, 3-stream slab pipeline, {s}-point host slab"}
+    out = {"value": args.points / dt, "unit": "gridpoints/s",
+           "h2d_bytes_per_step": h2d * dist.world, "d2h_bytes_per_step": d2h * dist.world,
+           "s_per_step": round(dt, 4), "steps": args.e2e_steps,
+           "path": "eval_program(pinned host fields) -> tlb_exec_host: H2D -> fused kernel "
+                   f"-> D2H, 3-stream slab pipeline, {s}-point host slab"}
+    out["link"] = link_floor(host["dg"].data, host["Gamma"].data, h2d, d2h, dt)
+    return out
+
+
+def link_floor(src, dst, h2d: int, d2h: int, s_per_step: float) -> dict:
+    """The e2e leg's roofline: this box's host<->device copy rates, measured
+    after the e2e timing on its own pinned slab (plain copies, no kernel),
+    H2D alone and D2H alone.  floor_s = max(H2D bytes / H2D rate, D2H bytes
+    / D2H rate): both directions concurrently at their solo rates (an ideal
+    full-duplex link) — a lower bound on any step that moves these bytes."""
+    import torch
+
+    nb = min(src.numel(), dst.numel(), 1 << 29)  # <= 4 GiB per direction
+    hs, hd = src.reshape(-1)[:nb], dst.reshape(-1)[:nb]
+    dev = torch.empty(nb, dtype=torch.float64, device="cuda")
+
+    def rate(fn, reps=2):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        return 8 * nb * reps / (time.perf_counter() - t0) / 1e9
+
+    up = rate(lambda: dev.copy_(hs, non_blocking=True))
+    down = rate(lambda: hd.copy_(dev, non_blocking=True))
+    floor = max(h2d / (up * 1e9), d2h / (down * 1e9))
+    del dev
+    torch.cuda.empty_cache()
+    return {"h2d_gbs": round(up, 2), "d2h_gbs": round(down, 2), "floor_s": round(floor, 4),
+            "frac": round(floor / s_per_step, 3),
+            "method": "pinned torch copies of up to 4 GiB per direction on this rank's e2e "
+                      "slab after the timed e2e steps (2 reps each); floor = max(H2D bytes / "
+                      "H2D rate, D2H bytes / D2H rate), i.e. an ideal full-duplex link"}
 
 
 def _host_view(f, lo, hi):

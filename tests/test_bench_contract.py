@@ -72,4 +72,7 @@ def test_our_arm_line():
     assert d["gpu_launches"] == 3
     assert d["e2e"]["h2d_bytes_per_step"] == 320 * (1 << 22)
     assert d["e2e"]["d2h_bytes_per_step"] == 192 * (1 << 22)
+    link = d["e2e"]["link"]  # the e2e leg's roofline: this box's copy rates
+    assert link["h2d_gbs"] > 1 and link["d2h_gbs"] > 1
+    assert 0 < link["frac"] <= 1.05 and link["floor_s"] > 0
     assert d["dtype"] == "f64" and d["higher_is_better"] is True
