@@ -118,6 +118,15 @@ int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
                const long long* pitches, int vec, int threads, long long max_blocks,
                void* stream);
 
+/* tlb_launch with the launch geometry the lowering chose for this kernel,
+ * read from its source (TLK_VEC, TLK_GRID_WAVES; the staged entry when the
+ * module has one): what a C caller without a tuning opinion should call —
+ * it is the shape the Python API, the host-staged path and the harness
+ * bindings launch (e.g. a one-shot grid of 1-point 128-thread blocks for
+ * the benchmark program).  Asynchronous on `stream`. */
+int tlb_launch_default(tlb_kernel* k, long long n, const void* const* field_bases,
+                       const long long* pitches, void* stream);
+
 /* Multi-domain batch: ndom subdomains, each with its own field bases
  * (field_bases[d*nfields+f]), pitches and point count ns[d].  The table is
  * resolved to per-slot pointers and uploaded once (synchronously, in the

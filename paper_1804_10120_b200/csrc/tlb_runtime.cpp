@@ -567,7 +567,9 @@ int resolve_slots(const tlb_kernel* k, const void* const* bases, const long long
 
 }  // namespace
 
-void tlb_internal_set_error(const char* msg) { g_err = std::string("tlb: ") + msg; }
+__attribute__((visibility("hidden"))) void tlb_internal_set_error(const char* msg) {
+  g_err = std::string("tlb: ") + msg;
+}
 
 // ================================================================ C-ABI ====
 
@@ -602,7 +604,7 @@ int tlb_device_sm_count(int* out) {
 // template's `#ifndef NAME / #define NAME <fallback expression>` defaults
 // never shadow an absent header define; a non-numeric value also yields
 // `dflt`.
-long long source_define(const char* src, const char* name, long long dflt) {
+static long long source_define(const char* src, const char* name, long long dflt) {
   const std::string key = std::string("#define ") + name + " ";
   const char* end = strstr(src, "// tlk_template.cuh");
   const char* p = strstr(src, key.c_str());
@@ -743,9 +745,9 @@ int tlb_kernel_attrs(tlb_kernel* k, const char* entry, int* regs, int* local_byt
 
 namespace {
 
-int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n, const uint64_t* slots,
-                bool vec2, int threads, long long max_blocks, CUstream stream,
-                bool stage = false) {
+static int launch_flat(tlb_kernel* k, Loaded* L, CtxState* st, long long n,
+                       const uint64_t* slots, bool vec2, int threads, long long max_blocks,
+                       CUstream stream, bool stage = false) {
   const size_t m = k->slot_field.size();
   // parameter block: { long long n; double* p[m]; } — passed by value
   std::vector<uint64_t> param(1 + m);
@@ -835,6 +837,19 @@ int tlb_launch(tlb_kernel* k, long long n, const void* const* field_bases,
   bool vec2 = vec == 2 ? true : (vec == 1 ? false : al);
   if (vec2 && !al) return fail("tlb_launch: vec=2 requested but a slot is not 16-byte aligned");
   return launch_flat(k, L, st, n, slots.data(), vec2, threads, max_blocks, (CUstream)stream);
+}
+
+int tlb_launch_default(tlb_kernel* k, long long n, const void* const* field_bases,
+                       const long long* pitches, void* stream) {
+  if (!k) return fail("tlb_launch_default: null kernel");
+  // the lowering's geometry from the source: TLK_VEC 2 = the 2-point entry
+  // where every slot is 16-byte aligned (vec 0), 1 = the 1-point entry; a
+  // staged module takes its staged entry; TLK_GRID_WAVES 0 = one-shot grid,
+  // w = w waves of resident blocks
+  const int vec = k->stage_threads > 0 ? 3 : (k->dflt_vec == 2 ? 0 : 1);
+  const long long mb = k->dflt_waves == 0 ? TLB_ONE_SHOT
+                                          : (k->dflt_waves > 1 ? -(long long)k->dflt_waves : 0);
+  return tlb_launch(k, n, field_bases, pitches, vec, 0, mb, stream);
 }
 
 int tlb_batch_create(tlb_kernel* k, int ndom, const void* const* field_bases,

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double* __restrict__ ou
 
 }  // namespace
 
-void tlb_internal_set_error(const char* msg);  // tlb_runtime.cpp
+__attribute__((visibility("hidden"))) void tlb_internal_set_error(const char* msg);  // tlb_runtime.cpp
 
 extern "C" int tlb_fp64_probe(double* out, int blocks, int iters, void* stream) {
   if (blocks < 1 || iters < 1) return 0;

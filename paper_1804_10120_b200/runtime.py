@@ -35,7 +35,7 @@ BASE_OPTIONS = (
 EXPORTED = (
     "tlb_abi_version", "tlb_init", "tlb_last_error", "tlb_nvrtc_version", "tlb_device_sm_count",
     "tlb_compile", "tlb_kernel_log", "tlb_kernel_cubin", "tlb_kernel_destroy",
-    "tlb_kernel_set_slots", "tlb_kernel_attrs", "tlb_launch",
+    "tlb_kernel_set_slots", "tlb_kernel_attrs", "tlb_launch", "tlb_launch_default",
     "tlb_batch_create",
     "tlb_batch_launch", "tlb_batch_destroy", "tlb_exec_host", "tlb_fill_uniform",
     "tlb_fp64_probe",
@@ -95,6 +95,8 @@ def lib() -> ctypes.CDLL:
                                              ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
                 "tlb_launch": (c_int, [c_vp, c_ll, ctypes.POINTER(c_vp), ctypes.POINTER(c_ll),
                                        c_int, c_int, c_ll, c_vp]),
+                "tlb_launch_default": (c_int, [c_vp, c_ll, ctypes.POINTER(c_vp),
+                                               ctypes.POINTER(c_ll), c_vp]),
                 "tlb_batch_create": (c_int, [c_vp, c_int, ctypes.POINTER(c_vp),
                                              ctypes.POINTER(c_ll), ctypes.POINTER(c_ll), c_vp,
                                              ctypes.POINTER(c_vp)]),

@@ -484,6 +484,30 @@ def test_statement_parts_are_bit_exact(name):
         _check(case, env_to_host(env2), want)
 
 
+@pytest.mark.parametrize("name", ["c4_p2", "c3_christoffel", "c2_maxwell", "c1_dtg"])
+def test_c_abi_default_launch_is_bit_exact(name):
+    # tlb_launch_default: the lowering's own geometry read from the source —
+    # what a C caller without tuning opinions calls
+    from paper_1804_10120_b200 import runtime
+    from paper_1804_10120_b200.evaluator import _bind, _fusion_plan
+
+    case = manifest()["cases"][name]
+    prog, vs = program(case["source"])
+    host, want = golden_io(name)
+    env = device_env(prog, host)
+    n, resizes = _fusion_plan(vs, env)
+    for lhs, size in resizes:
+        lhs.resize(size)
+    _, kern, stores = _bind(vs, env)
+    c_vp, c_ll = runtime.c_vp, runtime.c_ll
+    rc = runtime.lib().tlb_launch_default(
+        kern.handle, n, runtime._arr(c_vp, [s_.base for s_ in stores]),
+        runtime._arr(c_ll, [s_.pitch for s_ in stores]),
+        torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, runtime.lib().tlb_last_error()
+    _check(case, env_to_host(env), want)
+
+
 def test_grouped_program_in_a_multi_domain_batch():
     # contract3 lowers in output groups; its batch entry calls the same
     # group functions with the domain's slot pointers staged in shared memory

@@ -29,6 +29,20 @@ def test_library_exports_every_declared_symbol():
     assert lib.tlb_abi_version() == 1
 
 
+def test_library_exports_only_the_c_abi():
+    # the dynamic symbol table holds exactly the header's functions: internal
+    # helpers (launch geometry, source parsing, error plumbing) stay hidden
+    import shutil
+    import subprocess
+
+    if not shutil.which("nm"):
+        pytest.skip("no nm")
+    out = subprocess.run(["nm", "-D", "--defined-only", str(runtime.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    funcs = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    assert funcs == set(declared_symbols())
+
+
 def test_nvrtc_available_without_gpu():
     major, minor = runtime.nvrtc_version()
     assert (major, minor) >= (12, 8)
