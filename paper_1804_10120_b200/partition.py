@@ -64,10 +64,17 @@ def global_norm(fields: Sequence, group=None) -> float:
 
     partial = None
     for f in fields:
-        s = (f.data.to(torch.float64) ** 2).sum()
-        partial = s if partial is None else partial + s
-    if partial is None:
-        partial = torch.zeros((), dtype=torch.float64)
+        if f.data.numel() == 0:
+            continue
+        # one component array at a time (a dot product reduces in place: no
+        # full-size temporary, which a 2^28-point Gamma could not afford)
+        for row in f.data.to(torch.float64).reshape(-1, f.data.shape[-1]):
+            s = torch.dot(row, row)
+            partial = s if partial is None else partial + s
+    if partial is None:  # no fields on this rank: a zero on the backend's device
+        nccl = dist.is_available() and dist.is_initialized() and dist.get_backend(group) == "nccl"
+        partial = torch.zeros((), dtype=torch.float64,
+                              device="cuda" if nccl else "cpu")
     partial = partial.reshape(1)
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
