@@ -852,6 +852,21 @@ int tlb_launch_default(tlb_kernel* k, long long n, const void* const* field_base
   return tlb_launch(k, n, field_bases, pitches, vec, 0, mb, stream);
 }
 
+// $TLB_CACHE_DIR, else <directory of this library>/_kcache (created if
+// missing); empty when neither is usable
+static std::string harness_cache_dir() {
+  if (const char* e = getenv("TLB_CACHE_DIR")) return e;
+  Dl_info info;
+  if (!dladdr((void*)&tlb_harness_call, &info) || !info.dli_fname) return "";
+  std::string lib = info.dli_fname;
+  const size_t slash = lib.rfind('/');
+  std::string dir = (slash == std::string::npos ? std::string(".") : lib.substr(0, slash)) +
+                    "/_kcache";
+  mkdir(dir.c_str(), 0755);
+  struct stat sb;
+  return stat(dir.c_str(), &sb) == 0 && S_ISDIR(sb.st_mode) ? dir : "";
+}
+
 int tlb_batch_create(tlb_kernel* k, int ndom, const void* const* field_bases,
                      const long long* pitches, const long long* ns, void* stream,
                      tlb_batch** out) {
@@ -1164,9 +1179,14 @@ int tlb_harness_call(tlb_harness_kernel* hk, long n, double** const* tensors,
   {
     std::lock_guard<std::mutex> lk(mu);
     if (!hk->compiled) {
-      // optional on-disk cubin cache keyed by FNV-1a of source + options
+      // on-disk cubin cache keyed by FNV-1a of source + options: $TLB_CACHE_DIR,
+      // else the library's own kernel cache (<dir of libtlb200.so>/_kcache, the
+      // Python side's default too), where Registry.build_shared precompiles
+      // every entry — a harness process then loads cubins instead of running NVRTC
       std::string cache;
-      if (const char* dir = getenv("TLB_CACHE_DIR")) {
+      std::string dir_s = harness_cache_dir();
+      if (!dir_s.empty()) {
+        const char* dir = dir_s.c_str();
         uint64_t h = 1469598103934665603ull;
         auto mixin = [&h](const char* p) {
           for (; *p; ++p) h = (h ^ (unsigned char)*p) * 1099511628211ull;

@@ -175,7 +175,48 @@ class Registry:
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"{' '.join(cmd)}\n{res.stderr}")
+        precompile_harness(self.entries)
         return so
+
+
+def harness_source(v) -> str:
+    """The kernel source exactly as the bindings embed it (tl_src_NNNN:
+    every line newline-terminated, see _c_string)."""
+    return "".join(line + "\n" for line in lower_program([v]).source.split("\n"))
+
+
+def harness_cubin_name(source: str, opts) -> str:
+    """tlb_harness_call's cache file name: FNV-1a 64 over the source and each
+    option, each followed by a 0xff separator (tlb_runtime.cpp)."""
+    h = 1469598103934665603
+    for text in [source, *opts]:
+        for byte in text.encode():
+            h = ((h ^ byte) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+        h = ((h ^ 0xFF) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return f"harness_{h:016x}.cubin"
+
+
+def precompile_harness(entries) -> list[Path]:
+    """NVRTC-compile every entry's kernel into the cache the harness bindings
+    read ($TLB_CACHE_DIR, else the package's _kcache next to libtlb200.so),
+    so a harness process loads cubins instead of compiling (no GPU needed)."""
+    import ctypes
+
+    from .runtime import cache_dir, check, lib
+
+    opts = compile_options()
+    copts = (ctypes.c_char_p * len(opts))(*[o.encode() for o in opts])
+    out = []
+    for e in entries:
+        src = harness_source(e.stmt)
+        path = cache_dir() / harness_cubin_name(src, opts)
+        if not path.exists():
+            handle = ctypes.c_void_p()
+            check(lib().tlb_compile(src.encode(), copts, len(opts), str(path).encode(),
+                                    ctypes.byref(handle)), "tlb_compile")
+            lib().tlb_kernel_destroy(handle)
+        out.append(path)
+    return out
 
 
 # ------------------------------------------------------------ C rendering --

@@ -238,11 +238,17 @@ def test_reference_harness_drives_the_gpu_kernels(case, tmp_path):
     for v in vs:
         reg.register(v)
     so = reg.build_shared(tmp_path)
+    from paper_1804_10120_b200.runtime import cache_dir
+
+    before = set(cache_dir().glob("harness_*.cubin"))
     out = tmp_path / "out.tldf"
     res = subprocess.run([str(harness), str(so), str(tmp_path / "tloops_manifest.tsv"),
                           str(GOLDEN / f"{case}.in.tldf"), str(out)],
                          capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stderr
+    # build_shared precompiled every entry under the name the bindings look
+    # up: the harness process compiled nothing
+    assert set(cache_dir().glob("harness_*.cubin")) == before
     got, want = read_host(out), golden_io(case)[1]
     for t in spec["targets"]:
         assert same_bits(got[t], want[t]), t

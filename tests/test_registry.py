@@ -62,3 +62,28 @@ def test_dedup_and_ordinals():
     prog_text = tb.DTG + "dtg(sym<0,1>, i, j) = -2*alpha*K(i,j) + db(i,j) + db(j,i);\n"
     reg = _registry(prog_text)
     assert len(reg) == 1 and reg.entries[0].ordinal == 1
+
+
+def test_build_shared_precompiles_the_harness_cubins(tmp_path, monkeypatch):
+    # the bindings' tlb_harness_call looks its cubin up by FNV-1a of the
+    # embedded source + options; build_shared puts it there (no GPU needed)
+    import shutil
+
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.registry import Registry, harness_cubin_name, harness_source
+    from paper_1804_10120_b200.runtime import compile_options
+
+    if not shutil.which("cc"):
+        pytest.skip("no C compiler")
+    monkeypatch.setenv("TLB_CACHE_DIR", str(tmp_path / "cache"))
+    (tmp_path / "cache").mkdir()
+    _, vs = tb.load(tb.P2)
+    reg = Registry()
+    for v in vs:
+        reg.register(v)
+    reg.build_shared(tmp_path / "gen")
+    names = {harness_cubin_name(harness_source(v), compile_options()) for v in vs}
+    assert {p.name for p in (tmp_path / "cache").glob("harness_*.cubin")} == names
+    # the bindings embed exactly that source text
+    text = (tmp_path / "gen" / "tloops_bindings_b200.c").read_text()
+    assert text.count("static const char tl_src_") == len(vs)
