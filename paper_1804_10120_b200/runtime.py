@@ -291,6 +291,8 @@ class Kernel:
 
     def exec_host(self, n: int, comp_ptrs: Sequence[Sequence[int]], stream: int,
                   slab: int = 0) -> None:
+        if not slab:  # tuning: TLB_HOST_SLAB points per pipeline stage (0 = the runtime's)
+            slab = int(os.environ.get("TLB_HOST_SLAB", "0"))
         rows = [_arr(c_vp, list(r)) for r in comp_ptrs]
         outer = (ctypes.POINTER(c_vp) * len(rows))(
             *[ctypes.cast(r, ctypes.POINTER(c_vp)) for r in rows])
