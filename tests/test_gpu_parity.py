@@ -660,10 +660,15 @@ def test_parameter_block_beyond_4kib():
         assert same_bits(env_to_host(e)["A"], want["A"])
 
 
+@pytest.mark.parametrize("split", [0, 1])
 @pytest.mark.parametrize("bvec", [1, 2])
 @pytest.mark.parametrize("bptrs", [0, 1])
-@pytest.mark.parametrize("name", ["c4_p2", "c4_p3", "c1_dtg_odd", "seq_augmented"])
-def test_batch_entry_variants_bit_exact(name, bptrs, bvec):
+@pytest.mark.parametrize("name", ["c4_p2", "c4_p3", "c1_dtg_odd", "seq_augmented",
+                                  "c2_maxwell"])
+def test_batch_entry_variants_bit_exact(name, bptrs, bvec, split):
+    # split = 1: statement parts in the flat entry and (batch_split) as
+    # (part, domain) row runs of the 1-point batch entry — programs of one
+    # part lower unsplit
     from paper_1804_10120_b200.evaluator import _bind, _fusion_plan
     from paper_1804_10120_b200.lowering import Variant, lower_program
     from paper_1804_10120_b200.runtime import Batch, Kernel
@@ -682,7 +687,8 @@ def test_batch_entry_variants_bit_exact(name, bptrs, bvec):
         bases.append([s.base for s in stores])
         pitches.append([s.pitch for s in stores])
         ns.append(fp[0])
-    plan = lower_program(vs, variant=Variant(batch_ptrs=bptrs, batch_vec=bvec))
+    plan = lower_program(vs, variant=Variant(batch_ptrs=bptrs, batch_vec=bvec, split=split,
+                                             batch_split=split))
     kern = Kernel(plan)
     stream = torch.cuda.current_stream().cuda_stream
     Batch(kern, bases, pitches, ns, stream).launch(stream)
