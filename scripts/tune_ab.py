@@ -205,6 +205,11 @@ def main():
             "policy": {}, "nosplit": {"split": 0}, "split_t128": {"threads": 128},
             "split_t256": {"threads": 256}, "split_t512": {"threads": 512}}}
             for n in sizes for nm in ("p2", "c2_maxwell")]
+    if os.environ.get("SPLIT_MINB"):  # register caps (launch-bound min blocks) of split P2
+        sizes = [int(x) for x in os.environ["SPLIT_MINB"].split(",")]
+        cases = [{"program": "p2", "n": n, "variants": {
+            "policy": {}, "minb6": {"minb": 6}, "minb7": {"minb": 7}, "minb8": {"minb": 8}}}
+            for n in sizes]
     if os.environ.get("VNGROUPS"):  # output groups (Variant.vn) for the contractions
         sizes = [int(x) for x in os.environ["VNGROUPS"].split(",")]
         cases = [{"program": nm, "n": n, "variants": {
