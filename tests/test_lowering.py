@@ -363,3 +363,28 @@ def test_split_kernel_compiles_with_fewer_registers():
         raise AssertionError("no tlk_flat_v1")
 
     assert regs(plan) < regs(flat)
+
+
+@pytest.mark.parametrize("name", ["c1_dtg", "c2_maxwell", "c3_christoffel", "p2", "p3"])
+def test_c_abi_default_geometry_matches_the_python_launch(name):
+    # tlb_launch_default reads TLK_VEC / TLK_GRID_WAVES (and a staged ring)
+    # from the source; the Python Kernel launches the plan's variant: the two
+    # must name the same entry and grid (tlb_runtime.cpp tlb_launch_default)
+    import re
+
+    from paper_1804_10120_b200 import bench as tb
+    from paper_1804_10120_b200.runtime import ONE_SHOT, Kernel
+
+    _, vs = tb.load(tb.PROGRAMS[name])
+    plan = lower_program(vs)
+    k = Kernel(plan)
+
+    def define(key, dflt):
+        m = re.search(rf"^#define {key} (\S+)", plan.source, re.M)
+        return int(m.group(1)) if m else dflt
+
+    waves = define("TLK_GRID_WAVES", 1)
+    staged = define("TLK_NSTAGE", 0) > 0
+    c_vec = 3 if staged else (0 if define("TLK_VEC", 2) == 2 else 1)
+    c_mb = ONE_SHOT if waves == 0 else (-waves if waves > 1 else 0)
+    assert (k.vec, k.max_blocks) == (c_vec, c_mb)
