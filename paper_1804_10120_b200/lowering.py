@@ -951,10 +951,16 @@ def lower_program(statements: Sequence[Any], alias: Mapping[str, str] | None = N
         # concurrent DRAM streams each (the other entries run the parts in turn)
         fused = b  # the whole program's body: tlk_point, for every other entry
         low2, lhs2 = lower(0, parts, layout_of=low)
-        if low2.b.slots == fused.slots and low2.b.slot_flags == fused.slot_flags:
-            low, lhs_fields, b = low2, lhs2, low2.b
-        else:  # one parameter block must serve both bodies; never expected
+        if low2.b.slots != fused.slots or low2.b.slot_flags != fused.slot_flags:
+            # one parameter block must serve both bodies; never expected
             variant = Variant(**{**variant.__dict__, "split": 0})
+        elif policy and (min(_group_arrays(low2.b.instrs)) * variant.threads * 8
+                         < SPLIT_MIN_BLOCK_BYTES):
+            # a part that streams only a few arrays would run a full grid of
+            # blocks with little work each: keep such programs fused
+            variant = Variant(**{**variant.__dict__, "split": 0})
+        else:
+            low, lhs_fields, b = low2, lhs2, low2.b
     if hoist_loads is not None:
         variant = Variant(**{**variant.__dict__, "hoist": hoist_loads})
     if variant.ldmode == 1 and rw:
@@ -1086,6 +1092,29 @@ def _max_live(instrs: list[Instr]) -> int:
             if ins.dst not in last:  # never used
                 live -= 1
     return peak
+
+
+# policy 3 splits a program into statement parts only when every part moves
+# at least this many bytes per block (arrays x threads x 8 B, one point per
+# thread).  Measured (profiles/r02/tuning/tune_ab_split*.jsonl, split vs
+# fused at 2^24 / 2^26): Gamma + a 1-component copy (2 KB per 128-thread
+# block) -13 %, + a vector copy (6 KB) -10 %, + a 3x3 copy (18 KB) -1 to -2 %;
+# P2 (its smaller part: 22 arrays, 22.5 KB) +0.4-1.6 %, Maxwell (13 arrays in
+# 512-thread blocks, 53 KB) +0.2-1.5 %
+SPLIT_MIN_BLOCK_BYTES = 20480
+
+
+def _group_arrays(instrs: list[Instr]) -> list[int]:
+    """Distinct slots loaded or stored per 'grp'-separated group."""
+    out, cur = [], set()
+    for ins in instrs:
+        if ins.op == "grp":
+            out.append(len(cur))
+            cur = set()
+        elif ins.op in ("ld", "st"):
+            cur.add(ins.slot)
+    out.append(len(cur))
+    return out
 
 
 def statement_parts(statements: Sequence[Any], alias: Mapping[str, str] | None = None
