@@ -18,6 +18,7 @@ import csv
 import json
 import time
 from dataclasses import dataclass
+from pathlib import Path
 from statistics import median
 from typing import Callable, Iterable, Sequence
 
@@ -32,6 +33,8 @@ DEFAULT_SEED = 0xC0FFEE
 DEFAULT_GRIDS = (32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536)
 MODES = ("whole-tensor", "per-component")
 CSV_COLUMNS = ("name", "mode", "N", "t_median_s", "bw_eff_gbps", "N_e", "N_d")
+# --extended (SURVEY.md §5 metrics row): the device-side columns appended
+EXT_COLUMNS = ("gpus", "points_per_s", "hbm_gbps", "roofline_frac", "fp64_frac")
 
 # ------------------------------------------------- BASELINE.json programs --
 
@@ -114,9 +117,18 @@ class BenchResult:
     bw_eff: float  # GB/s
     n_e: int
     n_d: int
+    bytes_per_point: int = 0  # algorithmic roofline bytes (read-modify-write twice)
+    flops_per_point: int = 0
 
     def row(self) -> tuple:
         return (self.name, self.mode, self.gridsize, self.t, self.bw_eff, self.n_e, self.n_d)
+
+    def extended_row(self, hbm_peak_gbs: float, fp64_peak_gflops: float) -> tuple:
+        """EXT_COLUMNS: one GPU; points/s; algorithmic HBM GB/s and its
+        fraction of the copy peak; achieved fp64 GFLOP/s over the fp64 peak."""
+        hbm = self.bytes_per_point * self.gridsize / self.t / 1e9
+        fl = self.flops_per_point * self.gridsize / self.t / 1e9
+        return (1, self.gridsize / self.t, hbm, hbm / hbm_peak_gbs, fl / fp64_peak_gflops)
 
 
 def bw_eff(n_e: int, n_d: int, gridsize: int, t: float) -> float:
@@ -298,7 +310,11 @@ def run(entry: SuiteEntry, gridsize: int, *, reps: int = 21, mode: str = "whole-
     vstmt, env = entry.build_env(gridsize, seed)
     n_e, n_d = count_data(vstmt)
     t = time_statement(vstmt, env, reps=reps, mode=mode, clock=clock)
-    return BenchResult(entry.name, mode, gridsize, t, bw_eff(n_e, n_d, gridsize, t), n_e, n_d)
+    from .evaluator import plan_for
+
+    plan = plan_for(vstmt, env)
+    return BenchResult(entry.name, mode, gridsize, t, bw_eff(n_e, n_d, gridsize, t), n_e, n_d,
+                       plan.bytes_per_point, plan.flops_per_point)
 
 
 def sweep(entries: Sequence[SuiteEntry], gridsizes: Sequence[int] = DEFAULT_GRIDS, *,
@@ -308,14 +324,54 @@ def sweep(entries: Sequence[SuiteEntry], gridsizes: Sequence[int] = DEFAULT_GRID
             for e in entries for m in modes for n in gridsizes]
 
 
-def write_csv(results: Iterable[BenchResult], out) -> None:
-    """CSV with the reference's columns (bench.py:307-312)."""
+def write_csv(results: Iterable[BenchResult], out, peaks: tuple[float, float] | None = None
+              ) -> None:
+    """CSV with the reference's columns (bench.py:307-312); with `peaks`
+    (HBM GB/s, fp64 GFLOP/s) the EXT_COLUMNS appended."""
     w = csv.writer(out)
-    w.writerow(CSV_COLUMNS)
+    w.writerow(CSV_COLUMNS + (EXT_COLUMNS if peaks else ()))
     for r in results:
-        w.writerow([r.name, r.mode, r.gridsize, repr(r.t), repr(r.bw_eff), r.n_e, r.n_d])
+        row = [r.name, r.mode, r.gridsize, repr(r.t), repr(r.bw_eff), r.n_e, r.n_d]
+        if peaks:
+            row += [repr(x) for x in r.extended_row(*peaks)]
+        w.writerow(row)
 
 
-def write_json(results: Iterable[BenchResult], out) -> None:
-    json.dump([dict(zip(CSV_COLUMNS, r.row())) for r in results], out, indent=2)
+def write_json(results: Iterable[BenchResult], out, peaks: tuple[float, float] | None = None
+               ) -> None:
+    rows = []
+    for r in results:
+        d = dict(zip(CSV_COLUMNS, r.row()))
+        if peaks:
+            d.update(zip(EXT_COLUMNS, r.extended_row(*peaks)))
+        rows.append(d)
+    json.dump(rows, out, indent=2)
     out.write("\n")
+
+
+def device_peaks() -> tuple[float, float]:
+    """(HBM GB/s, fp64 GFLOP/s) for the extended columns: MEASURED_PEAKS.json
+    hbm_gbs when present (next to the package), else this box's device copy
+    rate measured now; the fp64 side from tlb_fp64_probe (uncontracted
+    DMUL + DADD, the kernels' instruction mix)."""
+    import torch
+
+    from .runtime import fp64_peak_gflops
+
+    p = Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json"
+    try:
+        hbm = float(json.loads(p.read_text())["hbm_gbs"])
+    except Exception:
+        a = torch.empty(1 << 28, dtype=torch.float64, device="cuda")
+        b = torch.empty_like(a)
+        b.copy_(a)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(5):
+            b.copy_(a)
+        e.record()
+        e.synchronize()
+        hbm = 5 * 2 * a.numel() * 8 / (s.elapsed_time(e) / 1e3) / 1e9
+        del a, b
+    return hbm, fp64_peak_gflops()

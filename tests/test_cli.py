@@ -91,3 +91,37 @@ def test_eval_stops_where_the_reference_stops(tmp_path):
     assert res.returncode == 1
     assert res.stderr == f"{f}: {spec['raises']['message']}\n"
     assert not out.exists()
+
+
+def test_bench_extended_row_arithmetic():
+    # SURVEY.md §5 metrics: the device columns appended by `bench --extended`
+    from paper_1804_10120_b200.bench import CSV_COLUMNS, EXT_COLUMNS, BenchResult
+
+    r = BenchResult("s1_dtg", "whole-tensor", 1 << 20, 1e-3, 0.0, 22, 1, 176, 24)
+    gpus, pts, hbm, frac, fp = r.extended_row(6455.0, 18400.0)
+    assert gpus == 1 and pts == (1 << 20) / 1e-3
+    assert hbm == 176 * (1 << 20) / 1e-3 / 1e9 and frac == hbm / 6455.0
+    assert fp == 24 * (1 << 20) / 1e-3 / 1e9 / 18400.0
+    assert len(CSV_COLUMNS + EXT_COLUMNS) == 12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extended", [False, True])
+def test_bench_subcommand_columns(tmp_path, extended):
+    import json
+    import subprocess
+    import sys
+
+    from paper_1804_10120_b200.bench import CSV_COLUMNS, DTG, EXT_COLUMNS
+
+    src = tmp_path / "dtg.tl"
+    src.write_text(DTG)
+    cmd = [sys.executable, "-m", "paper_1804_10120_b200", "bench", "--file", str(src),
+           "--grids", "4096", "--reps", "3", "--json"] + (["--extended"] if extended else [])
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr
+    (row,) = json.loads(res.stdout)
+    want = CSV_COLUMNS + (EXT_COLUMNS if extended else ())
+    assert tuple(row) == want
+    if extended:
+        assert row["gpus"] == 1 and row["points_per_s"] > 0 and 0 < row["roofline_frac"] < 2
