@@ -92,11 +92,17 @@ class Dist:
         if self.world > 1:
             import torch.distributed as dist
 
+            import datetime
+
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            # rank 0 times the CPU baselines (~1 min) while the others wait
+            # in a barrier: a timeout well beyond that
+            tmo = datetime.timedelta(minutes=30)
             if backend == "nccl":
-                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local),
+                                        timeout=tmo)
             else:
-                dist.init_process_group("gloo")
+                dist.init_process_group("gloo", timeout=tmo)
             self.pg = dist
 
     def barrier(self):
